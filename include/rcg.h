@@ -1,0 +1,212 @@
+/*
+ * rcg.h — C ABI of the B200-native augmented-PCG / Ritz-recycling hot path.
+ *
+ * The reference ("recycg", /root/reference/pkg/src/recycg) is pure Python; its
+ * drop-in seams are the module-level functions that run_sequence resolves at
+ * call time.  Each entry point below replaces one of them;
+ * the Python package paper_1301_7530_b200 binds these with ctypes under the
+ * reference's own names (INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *  - every pointer argument is a DEVICE pointer unless its name ends in _host;
+ *  - dense matrices are column-major with an explicit leading dimension
+ *    (each column — one Krylov / augmentation vector — is contiguous);
+ *  - every call is asynchronous on the context's stream unless documented to
+ *    synchronize; calls on one context are not thread-safe, distinct contexts
+ *    are independent (no global mutable state: reference SPEC.md:179-180);
+ *  - return value: RCG_OK or an error code; rcg_last_error(ctx) has the text.
+ *  - reductions are deterministic (fixed-order two-stage trees, no fp64
+ *    atomics), so repeated runs are bitwise identical (reference
+ *    tests/test_cli.py:129-136 determinism contract).
+ */
+#ifndef RCG_H
+#define RCG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum rcg_status {
+  RCG_OK = 0,
+  RCG_ERR_CONTRACT = 1,       /* ContractViolation (core.py:18-19)          */
+  RCG_ERR_RANK_DEFICIENT = 2, /* RankDeficient(column) (core.py:22-27)      */
+  RCG_ERR_NUMERICAL = 3,      /* NumericalFailure (core.py:30-31)           */
+  RCG_ERR_CUDA = 4,
+  RCG_ERR_OOM = 5
+};
+
+/* numerical-failure kinds reported by rcg_trace_view.failure */
+enum rcg_failure {
+  RCG_FAIL_NONE = 0,
+  RCG_FAIL_RZ = 1,  /* "(r, z) <= 0: preconditioner or operator not SPD"  solver.py:229-230,:279-280 */
+  RCG_FAIL_WAW = 2  /* "(w, A w) <= 0: operator not SPD on search space"  solver.py:244-245 */
+};
+
+typedef struct rcg_ctx rcg_ctx;
+typedef struct rcg_trace rcg_trace;
+
+/* CSR operator, full symmetric pattern (SparseSpdMatrix, core.py:34-111).
+ * row_offsets is int32 when row_offsets_64 == 0, else int64; col_indices int32. */
+typedef struct {
+  int64_t n;
+  int64_t nnz;
+  const void* row_offsets;
+  int32_t row_offsets_64;
+  int32_t pad_;
+  const int32_t* col_indices;
+  const double* values;
+} rcg_csr;
+
+/* Deflation operator P = I - C G^{-1} (AC)^T, G = C^T A C (DeflationOperator,
+ * solver.py:63-97).  C and AC are n x n_c column-major (ld >= n); L is the
+ * lower Cholesky factor of G and Ginv = G^{-1}, both n_c x n_c (ld = n_c). */
+typedef struct {
+  int64_t n;
+  int64_t n_c;
+  const double* C;
+  int64_t ldc;
+  const double* AC;
+  int64_t ldac;
+  const double* L;
+  const double* Ginv;
+} rcg_deflation;
+
+/* SolveConfig (solver.py:125-139) plus the launch batch (iterations queued
+ * between two host polls of the device-side convergence flag; 0 = auto). */
+typedef struct {
+  double tol;
+  int64_t max_iters;
+  int32_t reorthogonalize;
+  int32_t trace_capture;
+  int32_t store_directions;
+  int32_t batch;
+} rcg_solve_cfg;
+
+/* Read-only view of a finished solve (SolveTrace, solver.py:142-162). */
+typedef struct {
+  int64_t n;
+  int64_t iterations;      /* m                                              */
+  int64_t n_betas;         /* m-1 if converged, m if stopped by max_iters    */
+  int32_t converged;
+  int32_t failure;         /* enum rcg_failure                               */
+  int32_t early_exit;      /* loop skipped: ||r0|| <= 1e-13 ||b|| (solver.py:217-219) */
+  int32_t pad_;
+  double r0_norm;
+  double b_norm;
+  const double* alphas;         /* [m]   device */
+  const double* betas;          /* [m]   device */
+  const double* rz_inner;       /* [m]   device */
+  const double* residual_norms; /* [m+1] device */
+  const double* Z;              /* z_0..z_{m-1} (trace_capture), ld = ld      */
+  const double* W;              /* w_0..w_{m-1} (reorth or store_directions)  */
+  const double* AW;             /* A w_j        (reorth)                      */
+  const double* R;              /* r_0..r_{m-1} (store_directions)            */
+  const double* waw;            /* (w_j, A w_j) [m] (reorth)                  */
+  int64_t ld;
+  double device_seconds;        /* GPU time of the iteration loop            */
+} rcg_trace_view;
+
+/* ---- context ------------------------------------------------------------ */
+int rcg_ctx_create(int device, void* cuda_stream, rcg_ctx** out);
+void rcg_ctx_destroy(rcg_ctx* ctx);
+int rcg_ctx_set_stream(rcg_ctx* ctx, void* cuda_stream);
+const char* rcg_last_error(const rcg_ctx* ctx);
+int rcg_version(void);
+int rcg_num_kernel_launches(const rcg_ctx* ctx, int64_t* out_host); /* launches issued by ctx */
+
+/* ---- operators (core.py) ------------------------------------------------- */
+/* y = A x  (spmv, core.py:114-119 / SparseSpdMatrix.__matmul__ core.py:110-111) */
+int rcg_spmv(rcg_ctx* ctx, const rcg_csr* A, const double* x, double* y);
+/* Y = A X for k column-major columns (A @ C in build_deflation, solver.py:113) */
+int rcg_spmm(rcg_ctx* ctx, const rcg_csr* A, const double* X, int64_t ldx,
+             int64_t k, double* Y, int64_t ldy);
+/* diag(A) and 1/diag(A) (SparseSpdMatrix.diagonal core.py:103-104,
+ * Preconditioner.jacobi solver.py:39-41); either output may be NULL.
+ * Returns RCG_ERR_CONTRACT if a diagonal entry is missing. */
+int rcg_csr_diagonal(rcg_ctx* ctx, const rcg_csr* A, double* diag, double* inv_diag);
+/* elementwise y = inv_diag * x (Preconditioner.apply, solver.py:50-54) */
+int rcg_diag_apply(rcg_ctx* ctx, int64_t n, const double* inv_diag, const double* x, double* y);
+
+/* ---- dense small kernels -------------------------------------------------- */
+/* G = X^T Y (a x b, ld = a); symmetrize != 0 -> G = 0.5 (G + G^T) (a == b) */
+int rcg_gemm_tn(rcg_ctx* ctx, int64_t n, int64_t a, int64_t b, const double* X,
+                int64_t ldx, const double* Y, int64_t ldy, double* G, int32_t symmetrize);
+/* Y = X Q  (X: n x m ld ldx; Q: m x s ld ldq; Y: n x s ld ldy) */
+int rcg_gemm_nn(rcg_ctx* ctx, int64_t n, int64_t m, int64_t s, const double* X,
+                int64_t ldx, const double* Q, int64_t ldq, double* Y, int64_t ldy);
+/* Guarded Cholesky (dense_cholesky, core.py:195-243): pivot d_j <= pivot_rtol *
+ * max(d_<j), d_j <= 0 or non-finite -> RCG_ERR_RANK_DEFICIENT, *bad_col_host = j.
+ * Also writes Ginv = G^{-1} when Ginv != NULL.  Synchronizes. */
+int rcg_dense_cholesky(rcg_ctx* ctx, const double* G, int64_t n, double pivot_rtol,
+                       double* L, double* Ginv, int64_t* bad_col_host);
+
+/* ---- deflation (solver.py:63-117) ---------------------------------------- */
+/* AC = A C; G = sym(C^T AC); L = chol(G) with pivot_rtol 1e-12; Ginv = G^{-1}.
+ * RCG_ERR_RANK_DEFICIENT with *bad_col_host on a guarded pivot.  Synchronizes. */
+int rcg_deflation_build(rcg_ctx* ctx, const rcg_csr* A, const double* C, int64_t ldc,
+                        int64_t n_c, double* AC, int64_t ldac, double* L, double* Ginv,
+                        int64_t* bad_col_host);
+/* out = P x (DeflationOperator.project, solver.py:84-91) */
+int rcg_project(rcg_ctx* ctx, const rcg_deflation* D, const double* x, double* out);
+/* x0 = C G^{-1} C^T b (DeflationOperator.initial_guess, solver.py:93-97) */
+int rcg_initial_guess(rcg_ctx* ctx, const rcg_deflation* D, const double* b, double* x0);
+
+/* ---- APCG solve (apcg_solve, solver.py:193-290) --------------------------- */
+/* inv_diag == NULL -> identity preconditioner.  x receives the solution.
+ * On RCG_OK or RCG_ERR_NUMERICAL a trace is returned in *trace_out (free with
+ * rcg_trace_free); the NumericalFailure kind is in its view.  Synchronizes. */
+int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag,
+                   const rcg_deflation* D, const double* b, double* x,
+                   const rcg_solve_cfg* cfg, rcg_trace** trace_out);
+int rcg_trace_get_view(const rcg_trace* trace, rcg_trace_view* out_host);
+void rcg_trace_free(rcg_trace* trace);
+
+/* ---- Ritz extraction / selection (ritz.py:61-138, recycle.py:157-175) ----- */
+/* Lanczos tridiagonal d[m], e[m-1] from CG coefficients (lanczos_tridiag,
+ * ritz.py:61-78).  RCG_ERR_NUMERICAL if some beta < 0.  Synchronizes. */
+int rcg_lanczos_tridiag(rcg_ctx* ctx, const double* alphas, const double* betas,
+                        int64_t m, double* d, double* e);
+/* All eigenvalues of the symmetric tridiagonal (d, e), descending
+ * (tridiag_eig values, core.py:169-177) by Sturm bisection. */
+int rcg_tridiag_eigvals(rcg_ctx* ctx, const double* d, const double* e, int64_t m,
+                        double* values_desc);
+/* Eigenvectors for k requested descending indices idx[k] (device int64) of
+ * (d, e) whose eigenvalues values_desc are given: Q is m x k (ld m).
+ * Inverse iteration with in-cluster reorthogonalization. */
+int rcg_tridiag_eigvecs(rcg_ctx* ctx, const double* d, const double* e, int64_t m,
+                        const double* values_desc, const int64_t* idx, int64_t k,
+                        double* Q);
+/* Stagnation selection (select_converged, ritz.py:103-138) on device:
+ * mask[m] (uint8) from cur[m], prev[m-1] (both descending). */
+int rcg_select_converged(rcg_ctx* ctx, const double* cur, const double* prev, int64_t m,
+                         double epsilon, uint8_t* mask);
+/* One call for select_spectrum's numeric part (recycle.py:157-175 minus the
+ * cluster filter): tridiagonal from (alphas, betas), Ritz values of H_m and
+ * H_{m-1}, and the stagnation mask.  values[m], prev[max(m-1,1)], mask[m].
+ * Synchronizes (RCG_ERR_NUMERICAL on beta < 0). */
+int rcg_ritz_select(rcg_ctx* ctx, const double* alphas, const double* betas, int64_t m,
+                    double epsilon, double* d_work, double* e_work,
+                    double* values, double* prev, uint8_t* mask);
+/* Ritz vectors y_i = V q_{idx_i} with V = [(-1)^j z_j / sqrt(rz_j)] (ritz.py:
+ * 81-100), scaled by 1/sqrt(|theta_i|) when scale_by_theta != 0 (the SRKS
+ * block, recycle.py:151), written to Y (n x k, ld ldy).  Forms only the k
+ * requested columns: one skinny Z x Qtilde GEMM. */
+int rcg_ritz_vectors(rcg_ctx* ctx, const double* alphas, const double* betas,
+                     const double* rz, int64_t m, const double* Z, int64_t ldz,
+                     int64_t n, const double* values_desc, const int64_t* idx,
+                     int64_t k, int32_t scale_by_theta, double* Y, int64_t ldy);
+
+/* ---- TRKS block (update_basis_trks, recycle.py:127-140) ------------------ */
+/* column 2-norms of X (n x k) into norms[k] */
+int rcg_column_norms(rcg_ctx* ctx, int64_t n, int64_t k, const double* X, int64_t ldx,
+                     double* norms);
+/* Y[:, i] = X[:, i] / s[i] */
+int rcg_scale_columns(rcg_ctx* ctx, int64_t n, int64_t k, const double* X, int64_t ldx,
+                      const double* s, double* Y, int64_t ldy);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RCG_H */

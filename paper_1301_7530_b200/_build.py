@@ -1,0 +1,48 @@
+"""Build the in-tree CUDA library ``librcg.so`` for sm_100a with nvcc.
+
+The library is built in-tree (``paper_1301_7530_b200/librcg.so``) so it travels
+to the GPU box with the repo snapshot; nothing is JIT-compiled at import time.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+LIB = PKG / "librcg.so"
+SOURCES = ["api.cu", "spmv.cu", "dense.cu", "pcg.cu", "ritz.cu"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nvcc():
+    cand = os.environ.get("NVCC") or "/usr/local/cuda/bin/nvcc"
+    return cand if Path(cand).exists() else "nvcc"
+
+
+def needs_rebuild():
+    if not LIB.exists():
+        return True
+    t = LIB.stat().st_mtime
+    deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "rcg.h"]
+    return any(p.exists() and p.stat().st_mtime > t for p in deps)
+
+
+def build(force=False, verbose=True, extra=()):
+    if not force and not needs_rebuild():
+        return LIB
+    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+           "-Xptxas", "-v" if os.environ.get("RCG_PTXAS_VERBOSE") else "-O3",
+           "-I", str(PKG.parent / "include"), "-o", str(LIB) + ".tmp",
+           *[str(CSRC / s) for s in SOURCES], *extra]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    os.replace(str(LIB) + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv)

@@ -1,0 +1,360 @@
+// Small/skinny dense fp64 kernels: X^T Y (coarse matrix C^T A C,
+// solver.py:113-114), X Q (Ritz vectors V Q, ritz.py:100), guarded Cholesky
+// (core.py:195-243) + explicit coarse inverse, column norms / scaling (TRKS,
+// recycle.py:127-140).
+//
+// These are bandwidth- or latency-bound at the shapes of the hot path
+// (n_c <= ~100, s <= ~100 selected Ritz vectors), so they are plain
+// smem-tiled CUDA-core fp64 kernels; tensor cores are not used (fp64 DMMA
+// would not change the bound).  Every reduction is fixed-order.
+#include "rcg_internal.cuh"
+#include "dense.cuh"
+
+#include <cmath>
+#include <vector>
+
+namespace rcg {
+
+// ---------------------------------------------------------------------------
+// G = X^T Y, split over rows (grid.z) into fixed-order partials
+
+constexpr int TN_T = 32;  // output tile edge
+
+__global__ void __launch_bounds__(256)
+gemm_tn_partial(int64_t n, int64_t a, int64_t b, const double* __restrict__ X, int64_t ldx,
+                const double* __restrict__ Y, int64_t ldy, int64_t chunk, double* __restrict__ P) {
+  __shared__ double Xs[32][TN_T + 1];
+  __shared__ double Ys[32][TN_T + 1];
+  const int t = threadIdx.x;
+  const int ia = t & 31;
+  const int ib0 = (t >> 5) * 4;
+  const int64_t a0 = (int64_t)blockIdx.x * TN_T, b0 = (int64_t)blockIdx.y * TN_T;
+  const int64_t r_begin = (int64_t)blockIdx.z * chunk;
+  const int64_t r_end = min(n, r_begin + chunk);
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += 32) {
+    // load 32 rows x 32 cols of X and Y (row index fastest -> coalesced)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int rr = t & 31, cc = (t >> 5) + 8 * q;
+      const int64_t row = r0 + rr;
+      Xs[rr][cc] = (row < r_end && a0 + cc < a) ? X[(a0 + cc) * ldx + row] : 0.0;
+      Ys[rr][cc] = (row < r_end && b0 + cc < b) ? Y[(b0 + cc) * ldy + row] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int rr = 0; rr < 32; ++rr) {
+      const double xv = Xs[rr][ia];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] += xv * Ys[rr][ib0 + q];
+    }
+    __syncthreads();
+  }
+  double* Pz = P + (size_t)blockIdx.z * a * b;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int64_t i = a0 + ia, jj = b0 + ib0 + q;
+    if (i < a && jj < b) Pz[jj * a + i] = acc[q];
+  }
+}
+
+__global__ void gemm_tn_reduce(int64_t a, int64_t b, int S, const double* __restrict__ P, double* G,
+                               int symmetrize) {
+  const int64_t total = a * b;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx % a, jj = idx / a;
+    double s = 0.0;
+    for (int z = 0; z < S; ++z) s += P[(size_t)z * total + idx];
+    if (symmetrize) {
+      double s2 = 0.0;
+      const int64_t tidx = i * a + jj;  // (jj, i)
+      for (int z = 0; z < S; ++z) s2 += P[(size_t)z * total + tidx];
+      s = 0.5 * (s + s2);
+    }
+    G[idx] = s;
+  }
+}
+
+int gemm_tn(Ctx* c, int64_t n, int64_t a, int64_t b, const double* X, int64_t ldx, const double* Y,
+            int64_t ldy, double* G, int symmetrize) {
+  if (a == 0 || b == 0) return RCG_OK;
+  const int64_t ta = ceil_div(a, TN_T), tb = ceil_div(b, TN_T);
+  int64_t S = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 1024), (2 * c->num_sms) / (ta * tb)));
+  if (S > 65535) S = 65535;
+  int64_t chunk = ceil_div(ceil_div(n, S), 32) * 32;
+  if (chunk == 0) chunk = 32;
+  S = std::max<int64_t>(1, ceil_div(n, chunk));
+  double* P = nullptr;
+  int rc = scratch(c, sizeof(double) * (size_t)S * a * b, (void**)&P);
+  if (rc) return rc;
+  dim3 grid((unsigned)ta, (unsigned)tb, (unsigned)S);
+  gemm_tn_partial<<<grid, 256, 0, c->stream>>>(n, a, b, X, ldx, Y, ldy, chunk, P);
+  RCG_LAUNCH_CHECK(c);
+  const int g = (int)std::min<int64_t>(ceil_div(a * b, 256), c->num_sms * 4);
+  gemm_tn_reduce<<<g, 256, 0, c->stream>>>(a, b, (int)S, P, G, symmetrize);
+  RCG_LAUNCH_CHECK(c);
+  return RCG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Y = X Q  (n x m) (m x s), tile 64 rows x 32 cols, k-slab 32
+
+__global__ void __launch_bounds__(256)
+gemm_nn_kernel(int64_t n, int64_t m, int64_t s, const double* __restrict__ X, int64_t ldx,
+               const double* __restrict__ Q, int64_t ldq, double* __restrict__ Y, int64_t ldy) {
+  __shared__ double Xs[32][64];
+  __shared__ double Qs[32][33];
+  const int t = threadIdx.x;
+  const int r = t & 63;
+  const int c0 = (t >> 6) * 8;
+  const int64_t row0 = (int64_t)blockIdx.x * 64;
+  const int64_t col0 = (int64_t)blockIdx.y * 32;
+  double acc[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+  for (int64_t k0 = 0; k0 < m; k0 += 32) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int kk = (t >> 6) + 4 * q;  // 0..31
+      const int64_t row = row0 + r;
+      Xs[kk][r] = (row < n && k0 + kk < m) ? X[(k0 + kk) * ldx + row] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int kk = t & 31, cc = (t >> 5) + 8 * q;
+      Qs[kk][cc] = (k0 + kk < m && col0 + cc < s) ? Q[(col0 + cc) * ldq + k0 + kk] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < 32; ++kk) {
+      const double xv = Xs[kk][r];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] += xv * Qs[kk][c0 + q];
+    }
+    __syncthreads();
+  }
+  const int64_t row = row0 + r;
+  if (row < n) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (col0 + c0 + q < s) Y[(col0 + c0 + q) * ldy + row] = acc[q];
+  }
+}
+
+int gemm_nn(Ctx* c, int64_t n, int64_t m, int64_t s, const double* X, int64_t ldx, const double* Q,
+            int64_t ldq, double* Y, int64_t ldy) {
+  if (n == 0 || s == 0) return RCG_OK;
+  dim3 grid((unsigned)ceil_div(n, 64), (unsigned)ceil_div(s, 32));
+  gemm_nn_kernel<<<grid, 256, 0, c->stream>>>(n, m, s, X, ldx, Q, ldq, Y, ldy);
+  RCG_LAUNCH_CHECK(c);
+  return RCG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// guarded Cholesky.  Pivot rule of core.py:233-243 (and the LAPACK branch
+// core.py:226-232, which applies the same test to diag(L)^2):
+//   d_j <= pivot_rtol * max(d_0..d_{j-1})  or  d_j <= 0  or  !isfinite(d_j)
+//   -> RankDeficient(j) for the FIRST such j.
+
+constexpr int CHOL_SMEM_MAX = 128;
+
+// single CTA, whole matrix in shared memory (n <= 128), right-looking
+__global__ void __launch_bounds__(1024)
+chol_smem_kernel(int n, const double* __restrict__ G, double pivot_rtol, double* L, long long* bad) {
+  extern __shared__ double A[];  // n x n, column-major
+  __shared__ double s_piv;
+  __shared__ int s_bad;
+  const int t = threadIdx.x, nt = blockDim.x;
+  for (int idx = t; idx < n * n; idx += nt) A[idx] = G[idx];
+  if (t == 0) {
+    s_piv = 0.0;
+    s_bad = -1;
+  }
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    const double d = A[j * n + j];
+    const double top = s_piv;
+    if (d <= top * pivot_rtol || d <= 0.0 || !isfinite(d)) {
+      if (t == 0) s_bad = j;
+      break;  // uniform: every thread evaluates the same test
+    }
+    const double ljj = sqrt(d);
+    __syncthreads();
+    if (t == 0) s_piv = fmax(top, d);
+    for (int i = j + 1 + t; i < n; i += nt) A[j * n + i] /= ljj;
+    __syncthreads();
+    if (t == 0) A[j * n + j] = ljj;
+    // trailing update of the lower triangle
+    const int m = n - j - 1;
+    for (int idx = t; idx < m * m; idx += nt) {
+      const int kk = j + 1 + idx / m, i = j + 1 + idx % m;
+      if (i >= kk) A[kk * n + i] -= A[j * n + i] * A[j * n + kk];
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  for (int idx = t; idx < n * n; idx += nt) {
+    const int i = idx % n, kk = idx / n;
+    L[idx] = (i >= kk) ? A[idx] : 0.0;
+  }
+  if (t == 0) *bad = s_bad;
+}
+
+// global-memory left-looking column step for large n: column j of L
+// (launched once per column).  All blocks evaluate d_j identically.
+__global__ void __launch_bounds__(256)
+chol_col_kernel(int64_t n, int64_t j, const double* __restrict__ G, double* L, double* pivmax,
+                double pivot_rtol, long long* bad) {
+  if (*bad >= 0) return;
+  __shared__ double sm[8];
+  // d_j = G_jj - sum_k L_jk^2 (fixed-order block tree)
+  double part = 0.0;
+  for (int64_t k = threadIdx.x; k < j; k += blockDim.x) {
+    const double v = L[k * n + j];
+    part += v * v;
+  }
+  const double sumsq = block_sum<256>(part, sm);
+  const double d = G[j * n + j] - sumsq;
+  const double top = pivmax[j];
+  if (d <= top * pivot_rtol || d <= 0.0 || !isfinite(d)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *bad = j;
+    return;
+  }
+  const double ljj = sqrt(d);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    L[j * n + j] = ljj;
+    pivmax[j + 1] = fmax(top, d);
+  }
+  for (int64_t i = j + 1 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = G[j * n + i];
+    for (int64_t k = 0; k < j; ++k) s -= L[k * n + i] * L[k * n + j];
+    L[j * n + i] = s / ljj;
+  }
+}
+
+// Linv = L^{-1} (lower), one thread per column, forward substitution
+__global__ void trtri_lower_kernel(int64_t n, const double* __restrict__ L, double* Linv) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  for (int64_t i = 0; i < c; ++i) Linv[c * n + i] = 0.0;
+  for (int64_t i = c; i < n; ++i) {
+    double s = (i == c) ? 1.0 : 0.0;
+    for (int64_t k = c; k < i; ++k) s -= L[k * n + i] * Linv[c * n + k];
+    Linv[c * n + i] = s / L[i * n + i];
+  }
+}
+
+int cholesky(Ctx* c, const double* G, int64_t n, double pivot_rtol, double* L, double* Ginv,
+             int64_t* bad_col) {
+  *bad_col = -1;
+  if (n == 0) return RCG_OK;
+  // scratch layout: [bad (8 B) | pad | pivmax (n+1)]
+  const size_t need = 256 + sizeof(double) * (size_t)(n + 1);
+  char* base = nullptr;
+  int rc = scratch(c, need, (void**)&base);
+  if (rc) return rc;
+  long long* bad = (long long*)base;
+  double* pivmax = (double*)(base + 256);
+  if (n <= CHOL_SMEM_MAX) {
+    const size_t smem = sizeof(double) * (size_t)n * n;
+    RCG_CUDA(c, cudaFuncSetAttribute(chol_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)std::max<size_t>(smem, 48 * 1024)));
+    chol_smem_kernel<<<1, 1024, smem, c->stream>>>((int)n, G, pivot_rtol, L, bad);
+    RCG_LAUNCH_CHECK(c);
+  } else {
+    RCG_CUDA(c, cudaMemsetAsync(L, 0, sizeof(double) * (size_t)n * n, c->stream));
+    RCG_CUDA(c, cudaMemsetAsync(pivmax, 0, sizeof(double) * (size_t)(n + 1), c->stream));
+    RCG_CUDA(c, cudaMemsetAsync(bad, 0xff, sizeof(long long), c->stream));  // -1
+    for (int64_t j = 0; j < n; ++j) {
+      const int g = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n - j, 256), c->num_sms));
+      chol_col_kernel<<<g, 256, 0, c->stream>>>(n, j, G, L, pivmax, pivot_rtol, bad);
+      RCG_LAUNCH_CHECK(c);
+    }
+  }
+  long long hbad = -1;
+  RCG_CUDA(c, cudaMemcpyAsync(&hbad, bad, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  RCG_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (hbad >= 0) {
+    *bad_col = hbad;
+    return set_error(c, RCG_ERR_RANK_DEFICIENT, "non-positive pivot at column %lld", hbad);
+  }
+  if (Ginv) {
+    // Linv lives outside the ctx scratch because gemm_tn reuses the scratch
+    double* Linv = nullptr;
+    RCG_CUDA(c, cudaMallocAsync((void**)&Linv, sizeof(double) * (size_t)n * n, c->stream));
+    trtri_lower_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, c->stream>>>(n, L, Linv);
+    RCG_LAUNCH_CHECK(c);
+    rc = gemm_tn(c, n, n, n, Linv, n, Linv, n, Ginv, 1);   // Ginv = Linv^T Linv
+    cudaFreeAsync(Linv, c->stream);
+    if (rc) return rc;
+  }
+  return RCG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// column norms / scaling (update_basis_trks, recycle.py:127-140)
+
+__global__ void __launch_bounds__(256)
+colnorm_kernel(int64_t n, const double* __restrict__ X, int64_t ldx, double* norms) {
+  __shared__ double sm[8];
+  const double* x = X + (int64_t)blockIdx.x * ldx;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += x[i] * x[i];
+  s = block_sum<256>(s, sm);
+  if (threadIdx.x == 0) norms[blockIdx.x] = sqrt(s);
+}
+
+__global__ void scalecol_kernel(int64_t n, int64_t k, const double* __restrict__ X, int64_t ldx,
+                                const double* __restrict__ sdiv, double* Y, int64_t ldy) {
+  const int64_t col = blockIdx.y;
+  const double d = sdiv[col];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    Y[col * ldy + i] = X[col * ldx + i] / d;
+}
+
+}  // namespace rcg
+
+using namespace rcg;
+
+extern "C" int rcg_gemm_tn(rcg_ctx* ctx, int64_t n, int64_t a, int64_t b, const double* X, int64_t ldx,
+                           const double* Y, int64_t ldy, double* G, int32_t symmetrize) {
+  if (!ctx) return RCG_ERR_CONTRACT;
+  if (symmetrize && a != b) return set_error(ctx, RCG_ERR_CONTRACT, "symmetrize needs a square result");
+  return gemm_tn(ctx, n, a, b, X, ldx, Y, ldy, G, symmetrize);
+}
+
+extern "C" int rcg_gemm_nn(rcg_ctx* ctx, int64_t n, int64_t m, int64_t s, const double* X, int64_t ldx,
+                           const double* Q, int64_t ldq, double* Y, int64_t ldy) {
+  if (!ctx) return RCG_ERR_CONTRACT;
+  return gemm_nn(ctx, n, m, s, X, ldx, Q, ldq, Y, ldy);
+}
+
+extern "C" int rcg_dense_cholesky(rcg_ctx* ctx, const double* G, int64_t n, double pivot_rtol, double* L,
+                                  double* Ginv, int64_t* bad_col_host) {
+  if (!ctx) return RCG_ERR_CONTRACT;
+  int64_t bad = -1;
+  int rc = cholesky(ctx, G, n, pivot_rtol, L, Ginv, &bad);
+  if (bad_col_host) *bad_col_host = bad;
+  return rc;
+}
+
+extern "C" int rcg_column_norms(rcg_ctx* ctx, int64_t n, int64_t k, const double* X, int64_t ldx,
+                                double* norms) {
+  if (!ctx) return RCG_ERR_CONTRACT;
+  if (k == 0) return RCG_OK;
+  colnorm_kernel<<<(unsigned)k, 256, 0, ctx->stream>>>(n, X, ldx, norms);
+  RCG_LAUNCH_CHECK(ctx);
+  return RCG_OK;
+}
+
+extern "C" int rcg_scale_columns(rcg_ctx* ctx, int64_t n, int64_t k, const double* X, int64_t ldx,
+                                 const double* s, double* Y, int64_t ldy) {
+  if (!ctx) return RCG_ERR_CONTRACT;
+  if (k == 0 || n == 0) return RCG_OK;
+  dim3 grid((unsigned)std::min<int64_t>(ceil_div(n, 256), 64), (unsigned)k);
+  scalecol_kernel<<<grid, 256, 0, ctx->stream>>>(n, k, X, ldx, s, Y, ldy);
+  RCG_LAUNCH_CHECK(ctx);
+  return RCG_OK;
+}

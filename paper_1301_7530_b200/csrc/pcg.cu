@@ -1,0 +1,868 @@
+// Augmented (deflated) preconditioned CG for sm_100a — the iteration of
+// apcg_solve (/root/reference/pkg/src/recycg/solver.py:193-290) as five
+// fused, bandwidth-bound fp64 kernels per iteration:
+//
+//   K1 spmv      Aw_j = A w_j  (written straight into AW[:, j]) + (w_j, Aw_j)     :242-243
+//   K2 update    alpha = rz/wAw; x += alpha w; r -= alpha Aw; ||r||^2;
+//                AC^T (M^{-1} r) block partials (the projector's GEMV-T)          :246-258, :84-91
+//   K3 precond   ||r|| test (device flag); s = G^{-1} AC^T y; z = M^{-1} r - C s
+//                (written into Z[:, j+1]); (r, z); reorth partials AW^T z, AW^T w_j  :273-278
+//   K4 colreduce fixed-order reduction of the reorth partials (reorth only)
+//   K5 wupdate   beta = rz'/rz; w_{j+1} = z + beta w_j - W ((AW^T w)/diag)            :281-287
+//
+// Every kernel reads the iteration index j and a `done` flag from a device-
+// resident SolveState, so iterations are queued in batches with identical
+// launch parameters and the host polls convergence once per batch; kernels
+// queued past convergence / failure are no-ops.  The stopping iteration is
+// therefore exactly the reference's.  Elementwise updates use
+// explicitly non-fused multiply/add to match numpy's rounding; every reduction
+// is a fixed-order two-stage tree (bitwise reproducible run to run).
+#include "rcg_internal.cuh"
+#include "spmv.cuh"
+#include "dense.cuh"
+
+#include <algorithm>
+#include <chrono>
+#include <vector>
+
+namespace rcg {
+
+constexpr int CP_CHUNK = 4096;   // reorth coefficients staged per smem chunk
+constexpr int WU_RPT = 4;        // rows per thread in K5
+constexpr int NC_INLINE = 64;    // coarse solve recomputed per CTA up to this n_c
+
+struct IterArgs {
+  int64_t n;
+  const double* inv_diag;  // nullptr: identity preconditioner
+  // deflation
+  int64_t n_c;
+  const double* C;
+  int64_t ldc;
+  const double* AC;
+  int64_t ldac;
+  const double* Ginv;
+  double* s_ext;           // coarse solution when n_c > NC_INLINE
+  // vectors / histories
+  double* x;
+  double* r;
+  ColSel W, AW, Z, R;      // R.base == nullptr: no r history
+  double* waw_diag;
+  double* alphas;
+  double* betas;
+  double* rz_hist;
+  double* rnorms;
+  // reductions: sums[0] wAw | [1] rr | [2..2+n_c) AC^T y | [rz_off] rz | [rz_off+1+2k] AW_k^T z, [+1] AW_k^T w
+  double* sums;
+  int64_t rz_off;
+  double* part_upd;        // nb x (1 + n_c)
+  double* part_z;          // nb
+  double* part_reo;        // nb x reo_stride
+  int64_t reo_stride;
+  unsigned int* counters;  // [0] spmv [1] update [2] precond [3..] misc
+  SolveState* st;
+  int reorth;
+  int rows_per_block;
+};
+
+// ---------------------------------------------------------------------------
+// K2: alpha, x/r update, ||r||^2, AC^T y partials.  init != 0: no update
+// (initial residual: only ||r||^2 and AC^T y).
+
+__global__ void __launch_bounds__(kThreads)
+update_kernel(IterArgs a, int init) {
+  SolveState* st = a.st;
+  if (st->done) return;
+  const long long j = st->j;
+  double alpha = 0.0;
+  if (!init) {
+    const double wAw = a.sums[0];
+    const double rz = st->rz;
+    if (wAw <= 0.0) {                                       // solver.py:244-245
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->failure = RCG_FAIL_WAW;
+        st->done = 1;
+      }
+      return;
+    }
+    alpha = rz / wAw;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.alphas[j] = alpha;
+      a.rz_hist[j] = rz;
+      if (a.waw_diag) a.waw_diag[j] = wAw;
+    }
+  }
+  extern __shared__ double ytile[];
+  __shared__ double sm[kWarps];
+  const int64_t r0 = (int64_t)blockIdx.x * a.rows_per_block;
+  const int64_t r1 = min(a.n, r0 + a.rows_per_block);
+  const double* w = a.W.at(j);
+  const double* aw = a.AW.at(j);
+  double* rh = a.R.base ? a.R.at(j) : nullptr;
+  double rr = 0.0;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
+    double ri = a.r[i];
+    if (!init) {
+      if (rh) rh[i] = ri;
+      a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, w[i]));   // x = x + alpha w
+      ri = __dsub_rn(ri, __dmul_rn(alpha, aw[i]));          // r = r - alpha Aw
+      a.r[i] = ri;
+    }
+    rr += ri * ri;
+    if (a.n_c) ytile[i - r0] = a.inv_diag ? __dmul_rn(a.inv_diag[i], ri) : ri;
+  }
+  const int64_t K = 1 + a.n_c;
+  const double rrb = block_sum<kThreads>(rr, sm);
+  if (threadIdx.x == 0) a.part_upd[(size_t)blockIdx.x * K] = rrb;
+  if (a.n_c) {
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t len = r1 - r0;
+    for (int64_t c = wid; c < a.n_c; c += kWarps) {
+      const double* col = a.AC + c * a.ldac + r0;
+      double p0 = 0.0, p1 = 0.0;
+      int64_t i = lane;
+      for (; i + 32 < len; i += 64) {
+        p0 += col[i] * ytile[i];
+        p1 += col[i + 32] * ytile[i + 32];
+      }
+      if (i < len) p0 += col[i] * ytile[i];
+      const double p = warp_sum(p0 + p1);
+      if (lane == 0) a.part_upd[(size_t)blockIdx.x * K + 1 + c] = p;
+    }
+  }
+  if (arrive_last(a.counters + 1)) reduce_partials<kThreads>(a.part_upd, gridDim.x, (int)K, a.sums + 1);
+}
+
+// coarse solve s = G^{-1} (AC^T y) for n_c > NC_INLINE: one warp per row of Ginv
+__global__ void __launch_bounds__(kThreads)
+coarse_kernel(IterArgs a, int check_done) {
+  if (check_done && a.st->done) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= a.n_c) return;
+  const double* g = a.Ginv + row * a.n_c;   // symmetric: row == column
+  const double* u = a.sums + 2;
+  double s = 0.0;
+  for (int64_t k = lane; k < a.n_c; k += 32) s += g[k] * u[k];
+  s = warp_sum(s);
+  if (lane == 0) a.s_ext[row] = s;
+}
+
+// ---------------------------------------------------------------------------
+// K3: convergence test, z = M^{-1} r - C s, (r, z), reorth partials
+
+__global__ void __launch_bounds__(kThreads)
+precond_kernel(IterArgs a, int init) {
+  SolveState* st = a.st;
+  if (st->done) return;
+  const long long j = st->j;
+  if (!init) {
+    const double rnorm = sqrt(a.sums[1]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.rnorms[j + 1] = rnorm;
+    if (rnorm <= st->tol_abs) {                              // solver.py:273
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->converged = 1;
+        st->iterations = j + 1;
+        st->done = 1;
+      }
+      return;
+    }
+  }
+  extern __shared__ double dyn[];
+  __shared__ double sm[kWarps];
+  const int R = a.rows_per_block;
+  double* ztile = dyn;            // R
+  double* wtile = dyn + R;        // R
+  double* s = dyn + 2 * R;        // n_c
+  if (a.n_c) {
+    if (a.n_c <= NC_INLINE) {
+      // s_i = sum_k Ginv[i,k] u_k, fixed order (every CTA computes the same s)
+      const double* u = a.sums + 2;
+      for (int64_t i = threadIdx.x; i < a.n_c; i += kThreads) {
+        const double* g = a.Ginv + i * a.n_c;
+        double acc = 0.0;
+        for (int64_t k = 0; k < a.n_c; ++k) acc += g[k] * u[k];
+        s[i] = acc;
+      }
+    } else {
+      for (int64_t i = threadIdx.x; i < a.n_c; i += kThreads) s[i] = a.s_ext[i];
+    }
+    __syncthreads();
+  }
+  const int64_t r0 = (int64_t)blockIdx.x * R;
+  const int64_t r1 = min(a.n, r0 + R);
+  double* z = init ? a.Z.at(j) : a.Z.at(j + 1);
+  double* w0 = init ? a.W.at(j) : nullptr;
+  const double* wj = a.W.at(j);
+  const bool reo = a.reorth && !init;
+  double rz = 0.0;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
+    const double ri = a.r[i];
+    double zi = a.inv_diag ? __dmul_rn(a.inv_diag[i], ri) : ri;
+    if (a.n_c) {
+      double cs = 0.0;
+      for (int64_t c = 0; c < a.n_c; ++c) cs += a.C[c * a.ldc + i] * s[c];
+      zi = __dsub_rn(zi, cs);                               // y - C s  (solver.py:91)
+    }
+    z[i] = zi;
+    if (w0) w0[i] = zi;                                     // w_0 = z_0 (solver.py:231)
+    rz += ri * zi;
+    if (reo) {
+      ztile[i - r0] = zi;
+      wtile[i - r0] = wj[i];
+    }
+  }
+  const double rzb = block_sum<kThreads>(rz, sm);
+  if (threadIdx.x == 0) a.part_z[blockIdx.x] = rzb;
+  if (reo) {
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t len = r1 - r0;
+    double* prow = a.part_reo + (size_t)blockIdx.x * a.reo_stride;
+    for (long long k = wid; k <= j; k += kWarps) {
+      const double* col = a.AW.at(k) + r0;
+      double pz0 = 0.0, pz1 = 0.0, pw0 = 0.0, pw1 = 0.0;
+      int64_t i = lane;
+      for (; i + 32 < len; i += 64) {
+        const double c0 = col[i], c1 = col[i + 32];
+        pz0 += c0 * ztile[i];
+        pw0 += c0 * wtile[i];
+        pz1 += c1 * ztile[i + 32];
+        pw1 += c1 * wtile[i + 32];
+      }
+      if (i < len) {
+        const double c0 = col[i];
+        pz0 += c0 * ztile[i];
+        pw0 += c0 * wtile[i];
+      }
+      const double pz = warp_sum(pz0 + pz1);
+      const double pw = warp_sum(pw0 + pw1);
+      if (lane == 0) {
+        prow[2 * k] = pz;
+        prow[2 * k + 1] = pw;
+      }
+    }
+  }
+  if (arrive_last(a.counters + 2)) reduce_partials<kThreads>(a.part_z, gridDim.x, 1, a.sums + a.rz_off);
+}
+
+// K4: sums[rz_off+1+q] = sum_b part_reo[b][q], q < 2(j+1); 32 q per CTA x 8 b-groups
+__global__ void __launch_bounds__(256)
+colreduce_kernel(IterArgs a, int nb) {
+  if (a.st->done) return;
+  const long long j = a.st->j;
+  const int64_t Q = 2 * (j + 1);
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t q = (int64_t)blockIdx.x * 32 + tx;
+  __shared__ double sm[8][33];
+  double s = 0.0;
+  if (q < Q)
+    for (int b = ty; b < nb; b += 8) s += __ldcg(a.part_reo + (size_t)b * a.reo_stride + q);
+  sm[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && q < Q) {
+    double t = sm[0][tx];
+#pragma unroll
+    for (int g = 1; g < 8; ++g) t += sm[g][tx];
+    a.sums[a.rz_off + 1 + q] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5: beta, w_{j+1} = z + beta w_j  (- W c' with c' = (AW^T w)/diag)
+
+__global__ void __launch_bounds__(kThreads)
+wupdate_kernel(IterArgs a) {
+  SolveState* st = a.st;
+  if (st->done) return;
+  const long long j = st->j;
+  const double rz_new = a.sums[a.rz_off];
+  const double rz_old = st->rz;
+  if (rz_new <= 0.0) {                                       // solver.py:279-280
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->failure = RCG_FAIL_RZ;
+      st->done = 1;
+    }
+    return;
+  }
+  const double beta = rz_new / rz_old;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.betas[j] = beta;
+  __shared__ double cp[CP_CHUNK];
+  const int64_t r0 = (int64_t)blockIdx.x * (kThreads * WU_RPT);
+  const double* z = a.Z.at(j + 1);
+  const double* wo = a.W.at(j);
+  double* wn = a.W.at(j + 1);
+  double v[WU_RPT];
+#pragma unroll
+  for (int q = 0; q < WU_RPT; ++q) {
+    const int64_t i = r0 + threadIdx.x + q * kThreads;
+    v[q] = i < a.n ? __dadd_rn(z[i], __dmul_rn(beta, wo[i])) : 0.0;   // w = z + beta w
+  }
+  if (a.reorth) {
+    double acc[WU_RPT];
+#pragma unroll
+    for (int q = 0; q < WU_RPT; ++q) acc[q] = 0.0;
+    const double* red = a.sums + a.rz_off + 1;
+    for (long long k0 = 0; k0 <= j; k0 += CP_CHUNK) {
+      const long long kn = min((long long)CP_CHUNK, j + 1 - k0);
+      __syncthreads();
+      for (long long k = threadIdx.x; k < kn; k += kThreads) {
+        const long long kk = k0 + k;
+        // (AW^T (z + beta w))_k / (w_k, A w_k)   (solver.py:287)
+        cp[k] = (red[2 * kk] + beta * red[2 * kk + 1]) / a.waw_diag[kk];
+      }
+      __syncthreads();
+#pragma unroll 4
+      for (long long k = 0; k < kn; ++k) {
+        const double* col = a.W.at(k0 + k) + r0 + threadIdx.x;
+        const double ck = cp[k];
+#pragma unroll
+        for (int q = 0; q < WU_RPT; ++q)
+          if (r0 + threadIdx.x + q * kThreads < a.n) acc[q] += col[q * kThreads] * ck;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < WU_RPT; ++q) v[q] = __dsub_rn(v[q], acc[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < WU_RPT; ++q) {
+    const int64_t i = r0 + threadIdx.x + q * kThreads;
+    if (i < a.n) wn[i] = v[q];
+  }
+  if (arrive_last(a.counters + 4)) {
+    if (threadIdx.x == 0) {
+      st->rz = rz_new;
+      st->j = j + 1;
+      st->iterations = j + 1;
+    }
+  }
+}
+
+// initial (r0, z0) guard: rz <= 0 -> NumericalFailure before the loop (solver.py:229-230)
+__global__ void init_finish_kernel(IterArgs a) {
+  SolveState* st = a.st;
+  if (st->done) return;
+  const double rz = a.sums[a.rz_off];
+  if (rz <= 0.0) {
+    st->failure = RCG_FAIL_RZ;
+    st->done = 1;
+  } else {
+    st->rz = rz;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// generic GEMV-T (out[c] = X[:,c]^T v) with last-block reduction, and the
+// coarse combination out = base - sign * X (Ginv u)  (project / initial_guess)
+
+__global__ void __launch_bounds__(kThreads)
+gemv_t_kernel(int64_t n, int64_t k, const double* __restrict__ X, int64_t ldx, const double* __restrict__ v,
+              int rows_per_block, double* part, unsigned int* counter, double* out) {
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
+  const int64_t len = min(n, r0 + rows_per_block) - r0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int64_t c = wid; c < k; c += kWarps) {
+    const double* col = X + c * ldx + r0;
+    double p = 0.0;
+    for (int64_t i = lane; i < len; i += 32) p += col[i] * v[r0 + i];
+    p = warp_sum(p);
+    if (lane == 0) part[(size_t)blockIdx.x * k + c] = p;
+  }
+  if (arrive_last(counter)) reduce_partials<kThreads>(part, gridDim.x, (int)k, out);
+}
+
+__global__ void __launch_bounds__(kThreads)
+coarse_combine_kernel(int64_t n, int64_t n_c, const double* __restrict__ X, int64_t ldx,
+                      const double* __restrict__ Ginv, const double* __restrict__ u,
+                      const double* __restrict__ base, double* out) {
+  extern __shared__ double s[];
+  for (int64_t i = threadIdx.x; i < n_c; i += kThreads) {
+    const double* g = Ginv + i * n_c;
+    double acc = 0.0;
+    for (int64_t kk = 0; kk < n_c; ++kk) acc += g[kk] * u[kk];
+    s[i] = acc;
+  }
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
+    double cs = 0.0;
+    for (int64_t c = 0; c < n_c; ++c) cs += X[c * ldx + i] * s[c];
+    out[i] = base ? __dsub_rn(base[i], cs) : cs;
+  }
+}
+
+__global__ void copy_norms_kernel(int64_t n, const double* __restrict__ b, double* r, double* x,
+                                  double* part, unsigned int* counter, double* out) {
+  __shared__ double sm[kWarps];
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
+    const double bv = b[i];
+    r[i] = bv;
+    x[i] = 0.0;
+    s += bv * bv;
+  }
+  s = block_sum<kThreads>(s, sm);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = s;
+    part[2 * blockIdx.x + 1] = s;
+  }
+  if (arrive_last(counter)) reduce_partials<kThreads>(part, gridDim.x, 2, out);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+static int rows_per_block_for(const Ctx* c, int64_t n) {
+  int64_t rpt = ceil_div(n, (int64_t)kThreads * 2 * c->num_sms);
+  rpt = std::max<int64_t>(1, std::min<int64_t>(rpt, 16));
+  return (int)(rpt * kThreads);
+}
+
+int gemv_t(Ctx* c, int64_t n, int64_t k, const double* X, int64_t ldx, const double* v, double* out) {
+  if (k == 0) return RCG_OK;
+  const int R = rows_per_block_for(c, n);
+  const int nb = (int)std::max<int64_t>(1, ceil_div(n, R));
+  char* base = nullptr;
+  int rc = scratch(c, 256 + sizeof(double) * (size_t)nb * k, (void**)&base);
+  if (rc) return rc;
+  gemv_t_kernel<<<nb, kThreads, 0, c->stream>>>(n, k, X, ldx, v, R, (double*)(base + 256), c->counters + 8,
+                                               out);
+  RCG_LAUNCH_CHECK(c);
+  return RCG_OK;
+}
+
+int coarse_combine(Ctx* c, const rcg_deflation* D, const double* u, const double* base, double* out) {
+  const size_t smem = sizeof(double) * (size_t)std::max<int64_t>(D->n_c, 1);
+  if (smem > 48 * 1024)
+    RCG_CUDA(c, cudaFuncSetAttribute(coarse_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+  coarse_combine_kernel<<<elementwise_grid(c, D->n), kThreads, smem, c->stream>>>(D->n, D->n_c, D->C, D->ldc,
+                                                                                  D->Ginv, u, base, out);
+  RCG_LAUNCH_CHECK(c);
+  return RCG_OK;
+}
+
+}  // namespace rcg
+
+using namespace rcg;
+
+// ---------------------------------------------------------------------------
+// trace object (owns the device histories of one solve)
+
+struct rcg_trace {
+  rcg_trace_view view{};
+  std::vector<void*> allocs;
+  cudaStream_t stream = nullptr;
+  int device = 0;
+};
+
+extern "C" int rcg_trace_get_view(const rcg_trace* t, rcg_trace_view* out) {
+  if (!t || !out) return RCG_ERR_CONTRACT;
+  *out = t->view;
+  return RCG_OK;
+}
+
+extern "C" void rcg_trace_free(rcg_trace* t) {
+  if (!t) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(t->device);
+  cudaStreamSynchronize(t->stream);
+  for (void* p : t->allocs)
+    if (p) cudaFree(p);
+  cudaSetDevice(prev);
+  delete t;
+}
+
+namespace {
+
+struct Grow {
+  // a column-major history buffer that grows geometrically
+  double* ptr = nullptr;
+  int64_t cols = 0;
+};
+
+int grow(Ctx* c, Grow& g, int64_t need_cols, int64_t ld, int64_t used_cols) {
+  if (need_cols <= g.cols) return RCG_OK;
+  int64_t cols = std::max<int64_t>(need_cols, g.cols * 2);
+  double* p = nullptr;
+  cudaError_t e = cudaMalloc((void**)&p, sizeof(double) * (size_t)cols * ld);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    // retry at the exact requirement before giving up
+    cols = need_cols;
+    e = cudaMalloc((void**)&p, sizeof(double) * (size_t)cols * ld);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return set_error(c, RCG_ERR_OOM, "out of device memory growing a Krylov history to %lld columns (%.2f GB)",
+                       (long long)cols, 8.0 * cols * ld / 1e9);
+    }
+  }
+  if (g.ptr) {
+    if (used_cols > 0)
+      RCG_CUDA(c, cudaMemcpyAsync(p, g.ptr, sizeof(double) * (size_t)used_cols * ld, cudaMemcpyDeviceToDevice,
+                                  c->stream));
+    RCG_CUDA(c, cudaStreamSynchronize(c->stream));
+    cudaFree(g.ptr);
+  }
+  g.ptr = p;
+  g.cols = cols;
+  return RCG_OK;
+}
+
+}  // namespace
+
+extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, const rcg_deflation* D,
+                              const double* b, double* x, const rcg_solve_cfg* cfg, rcg_trace** trace_out) {
+  if (!ctx || !A || !cfg || !trace_out) return RCG_ERR_CONTRACT;
+  *trace_out = nullptr;
+  Ctx* c = ctx;
+  const int64_t n = A->n;
+  if (D && D->n != n) return set_error(c, RCG_ERR_CONTRACT, "deflation operator dimension mismatch");
+  if (!(cfg->tol > 0.0 && cfg->tol < 1.0)) return set_error(c, RCG_ERR_CONTRACT, "tol must be in (0, 1)");
+  if (cfg->max_iters < 1) return set_error(c, RCG_ERR_CONTRACT, "max_iters must be >= 1");
+  const int64_t n_c = D ? D->n_c : 0;
+  const int64_t ld = pad_ld(std::max<int64_t>(n, 1));
+  const bool reorth = cfg->reorthogonalize != 0;
+  const bool store = cfg->store_directions != 0;
+  const bool capture = cfg->trace_capture != 0;
+  const int64_t max_it = cfg->max_iters;
+
+  rcg_trace* T = new rcg_trace();
+  T->stream = c->stream;
+  T->device = c->device;
+  auto fail = [&](int rc) {
+    rcg_trace_free(T);
+    return rc;
+  };
+  auto alloc = [&](size_t bytes, void** p) -> int {
+    cudaError_t e = cudaMalloc(p, std::max<size_t>(bytes, 256));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return set_error(c, RCG_ERR_OOM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+    }
+    T->allocs.push_back(*p);
+    return RCG_OK;
+  };
+
+  const int R = rows_per_block_for(c, n);
+  const int nb = (int)std::max<int64_t>(1, ceil_div(n, R));
+  const int nbs = spmv_partials(c, A);
+
+  // fixed-size device allocations
+  SolveState* st = nullptr;
+  double *hist = nullptr, *r = nullptr, *sums = nullptr, *part_upd = nullptr, *part_z = nullptr;
+  double* part_spmv = nullptr;
+  double* s_ext = nullptr;
+  unsigned int* counters = nullptr;
+  const int64_t nh = max_it + 2;
+  int rc;
+  if ((rc = alloc(sizeof(SolveState), (void**)&st))) return fail(rc);
+  if ((rc = alloc(sizeof(double) * 5 * nh, (void**)&hist))) return fail(rc);
+  if ((rc = alloc(sizeof(double) * ld, (void**)&r))) return fail(rc);
+  if ((rc = alloc(sizeof(double) * nb * (1 + n_c), (void**)&part_upd))) return fail(rc);
+  if ((rc = alloc(sizeof(double) * (nb + 2 * nbs + 64), (void**)&part_z))) return fail(rc);
+  part_spmv = part_z + nb + 32;
+  if ((rc = alloc(sizeof(double) * (n_c + 1), (void**)&s_ext))) return fail(rc);
+  if ((rc = alloc(sizeof(unsigned int) * 16, (void**)&counters))) return fail(rc);
+  RCG_CUDA(c, cudaMemsetAsync(counters, 0, sizeof(unsigned int) * 16, c->stream));
+  RCG_CUDA(c, cudaMemsetAsync(hist, 0, sizeof(double) * 5 * nh, c->stream));
+  double* alphas = hist;
+  double* betas = hist + nh;
+  double* rzh = hist + 2 * nh;
+  double* rnorms = hist + 3 * nh;
+  double* wawd = hist + 4 * nh;
+
+  // growable histories
+  Grow gW, gAW, gZ, gR, gPR, gSum;
+  const bool storeW = reorth || store;
+  const int64_t init_cols = std::min<int64_t>(max_it + 2, 64);
+  if ((rc = grow(c, gW, storeW ? init_cols : 2, ld, 0))) return fail(rc);
+  if ((rc = grow(c, gAW, reorth ? init_cols : 1, ld, 0))) return fail(rc);
+  if ((rc = grow(c, gZ, capture ? init_cols : 2, ld, 0))) return fail(rc);
+  if (store && (rc = grow(c, gR, init_cols, ld, 0))) return fail(rc);
+
+  auto reo_cols = [&]() { return gAW.cols; };
+  auto ensure_sums = [&](void) -> int {
+    const int64_t need = 8 + n_c + 1 + 2 * reo_cols() + 8;
+    if (gSum.cols < need) {
+      double* p = nullptr;
+      cudaError_t e = cudaMalloc((void**)&p, sizeof(double) * need);
+      if (e != cudaSuccess) return set_error(c, RCG_ERR_OOM, "sums alloc");
+      RCG_CUDA(c, cudaMemsetAsync(p, 0, sizeof(double) * need, c->stream));
+      if (gSum.ptr) {
+        RCG_CUDA(c, cudaMemcpyAsync(p, gSum.ptr, sizeof(double) * gSum.cols, cudaMemcpyDeviceToDevice, c->stream));
+        RCG_CUDA(c, cudaStreamSynchronize(c->stream));
+        cudaFree(gSum.ptr);
+      }
+      gSum.ptr = p;
+      gSum.cols = need;
+    }
+    if (reorth) {
+      const int64_t needp = (int64_t)nb * 2 * reo_cols();
+      if (gPR.cols < needp) {
+        if (gPR.ptr) {
+          RCG_CUDA(c, cudaStreamSynchronize(c->stream));
+          cudaFree(gPR.ptr);
+        }
+        gPR.ptr = nullptr;
+        cudaError_t e = cudaMalloc((void**)&gPR.ptr, sizeof(double) * needp);
+        if (e != cudaSuccess) return set_error(c, RCG_ERR_OOM, "reorth partials alloc");
+        gPR.cols = needp;
+      }
+    }
+    return RCG_OK;
+  };
+  if ((rc = ensure_sums())) return fail(rc);
+
+  IterArgs a{};
+  auto refresh = [&]() {
+    a.n = n;
+    a.inv_diag = inv_diag;
+    a.n_c = n_c;
+    a.C = D ? D->C : nullptr;
+    a.ldc = D ? D->ldc : 0;
+    a.AC = D ? D->AC : nullptr;
+    a.ldac = D ? D->ldac : 0;
+    a.Ginv = D ? D->Ginv : nullptr;
+    a.s_ext = s_ext;
+    a.x = x;
+    a.r = r;
+    a.W = colsel(gW.ptr, ld, storeW ? 0 : 2);
+    a.AW = colsel(gAW.ptr, ld, reorth ? 0 : 1);
+    a.Z = colsel(gZ.ptr, ld, capture ? 0 : 2);
+    a.R = colsel(store ? gR.ptr : nullptr, ld, 0);
+    a.waw_diag = wawd;
+    a.alphas = alphas;
+    a.betas = betas;
+    a.rz_hist = rzh;
+    a.rnorms = rnorms;
+    a.sums = gSum.ptr;
+    a.rz_off = 2 + n_c;
+    a.part_upd = part_upd;
+    a.part_z = part_z;
+    a.part_reo = gPR.ptr;
+    a.reo_stride = 2 * reo_cols();
+    a.counters = counters;
+    a.st = st;
+    a.reorth = reorth ? 1 : 0;
+    a.rows_per_block = R;
+  };
+  refresh();
+
+  const size_t smem_upd = sizeof(double) * (n_c ? R : 1);
+  const size_t smem_pre = sizeof(double) * (2 * (size_t)R + n_c + 1);
+  RCG_CUDA(c, cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)std::max<size_t>(smem_upd, 1024)));
+  RCG_CUDA(c, cudaFuncSetAttribute(precond_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)std::max<size_t>(smem_pre, 1024)));
+
+  // ---- initial guess and residual (solver.py:208-219) ----
+  SolveState hs{};
+  hs.j = 0;
+  hs.iterations = 0;
+  hs.done = 0;
+  RCG_CUDA(c, cudaMemcpyAsync(st, &hs, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
+  double* norms2 = nullptr;  // ||r0||^2, ||b||^2
+  if ((rc = alloc(sizeof(double) * 16, (void**)&norms2))) return fail(rc);
+  if (n_c) {
+    // x0 = C G^{-1} C^T b; r0 = b - A x0
+    if ((rc = gemv_t(c, n, n_c, D->C, D->ldc, b, gSum.ptr + 2))) return fail(rc);
+    if ((rc = coarse_combine(c, D, gSum.ptr + 2, nullptr, x))) return fail(rc);
+    if ((rc = launch_spmv(c, A, 2, colsel(x), colsel(r), b, nullptr, part_spmv, counters + 0, norms2)))
+      return fail(rc);
+  } else {
+    copy_norms_kernel<<<elementwise_grid(c, n), kThreads, 0, c->stream>>>(n, b, r, x, part_spmv, counters + 0,
+                                                                        norms2);
+    RCG_LAUNCH_CHECK(c);
+  }
+  double hn[2] = {0.0, 0.0};
+  RCG_CUDA(c, cudaMemcpyAsync(hn, norms2, sizeof(hn), cudaMemcpyDeviceToHost, c->stream));
+  RCG_CUDA(c, cudaStreamSynchronize(c->stream));
+  const double r0 = std::sqrt(hn[0]);
+  const double bn = std::sqrt(hn[1]);
+  T->view.n = n;
+  T->view.r0_norm = r0;
+  T->view.b_norm = bn;
+  T->view.ld = ld;
+  RCG_CUDA(c, cudaMemcpyAsync(rnorms, &r0, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+
+  auto finish_view = [&](void) {
+    T->view.alphas = alphas;
+    T->view.betas = betas;
+    T->view.rz_inner = rzh;
+    T->view.residual_norms = rnorms;
+    T->view.Z = capture ? gZ.ptr : nullptr;
+    T->view.W = storeW ? gW.ptr : nullptr;
+    T->view.AW = reorth ? gAW.ptr : nullptr;
+    T->view.R = store ? gR.ptr : nullptr;
+    T->view.waw = wawd;
+    T->allocs.push_back(gW.ptr);
+    T->allocs.push_back(gAW.ptr);
+    T->allocs.push_back(gZ.ptr);
+    T->allocs.push_back(gR.ptr);
+    T->allocs.push_back(gPR.ptr);
+    T->allocs.push_back(gSum.ptr);
+    gW.ptr = gAW.ptr = gZ.ptr = gR.ptr = gPR.ptr = gSum.ptr = nullptr;
+  };
+
+  if (r0 == 0.0 || r0 <= 1e-13 * bn) {                     // solver.py:217-219
+    T->view.iterations = 0;
+    T->view.n_betas = 0;
+    T->view.converged = 1;
+    T->view.early_exit = 1;
+    finish_view();
+    *trace_out = T;
+    return RCG_OK;
+  }
+  hs.tol_abs = cfg->tol * r0;
+  RCG_CUDA(c, cudaMemcpyAsync(st, &hs, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
+
+  auto launch_coarse = [&](int check_done) -> int {
+    if (n_c > NC_INLINE) {
+      coarse_kernel<<<(unsigned)ceil_div(n_c * 32, kThreads), kThreads, 0, c->stream>>>(a, check_done);
+      RCG_LAUNCH_CHECK(c);
+    }
+    return RCG_OK;
+  };
+
+  // ---- z0, rz0, w0 (solver.py:221-231) ----
+  update_kernel<<<nb, kThreads, smem_upd, c->stream>>>(a, 1);
+  RCG_LAUNCH_CHECK(c);
+  if ((rc = launch_coarse(1))) return fail(rc);
+  precond_kernel<<<nb, kThreads, smem_pre, c->stream>>>(a, 1);
+  RCG_LAUNCH_CHECK(c);
+  init_finish_kernel<<<1, 1, 0, c->stream>>>(a);
+  RCG_LAUNCH_CHECK(c);
+
+  // ---- the loop (solver.py:241-288), batched ----
+  cudaEvent_t ev0, ev1;
+  cudaEventCreate(&ev0);
+  cudaEventCreate(&ev1);
+  cudaEventRecord(ev0, c->stream);
+  SolveState* hst = (SolveState*)c->pinned;
+  int64_t it = 0;
+  int64_t batch = cfg->batch > 0 ? cfg->batch : 4;
+  const int wu_grid = (int)std::max<int64_t>(1, ceil_div(n, (int64_t)kThreads * WU_RPT));
+  bool done = false;
+  while (it < max_it && !done) {
+    const int64_t B = std::min<int64_t>(batch, max_it - it);
+    // capacity for columns up to it + B + 1
+    const int64_t need = it + B + 2;
+    bool regrown = false;
+    if (storeW && need > gW.cols) {
+      if ((rc = grow(c, gW, need, ld, it + 1))) return fail(rc);
+      regrown = true;
+    }
+    if (reorth && need > gAW.cols) {
+      if ((rc = grow(c, gAW, need, ld, it + 1))) return fail(rc);
+      regrown = true;
+    }
+    if (capture && need > gZ.cols) {
+      if ((rc = grow(c, gZ, need, ld, it + 1))) return fail(rc);
+      regrown = true;
+    }
+    if (store && need > gR.cols) {
+      if ((rc = grow(c, gR, need, ld, it + 1))) return fail(rc);
+      regrown = true;
+    }
+    if (regrown) {
+      if ((rc = ensure_sums())) return fail(rc);
+      refresh();
+    }
+    for (int64_t q = 0; q < B; ++q) {
+      const int64_t jj = it + q;  // upper bound of the device-side j
+      if ((rc = launch_spmv(c, A, 1, a.W, a.AW, nullptr, st, part_spmv, counters + 0, gSum.ptr))) return fail(rc);
+      update_kernel<<<nb, kThreads, smem_upd, c->stream>>>(a, 0);
+      RCG_LAUNCH_CHECK(c);
+      if ((rc = launch_coarse(1))) return fail(rc);
+      precond_kernel<<<nb, kThreads, smem_pre, c->stream>>>(a, 0);
+      RCG_LAUNCH_CHECK(c);
+      if (reorth) {
+        colreduce_kernel<<<(unsigned)ceil_div(2 * (jj + 1), 32), 256, 0, c->stream>>>(a, nb);
+        RCG_LAUNCH_CHECK(c);
+      }
+      wupdate_kernel<<<wu_grid, kThreads, 0, c->stream>>>(a);
+      RCG_LAUNCH_CHECK(c);
+    }
+    it += B;
+    RCG_CUDA(c, cudaMemcpyAsync(hst, st, sizeof(SolveState), cudaMemcpyDeviceToHost, c->stream));
+    RCG_CUDA(c, cudaStreamSynchronize(c->stream));
+    done = hst->done != 0;
+    batch = std::min<int64_t>(batch * 2, 64);
+  }
+  cudaEventRecord(ev1, c->stream);
+  RCG_CUDA(c, cudaMemcpyAsync(hst, st, sizeof(SolveState), cudaMemcpyDeviceToHost, c->stream));
+  RCG_CUDA(c, cudaStreamSynchronize(c->stream));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ev0, ev1);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  T->view.device_seconds = ms * 1e-3;
+  T->view.failure = hst->failure;
+  T->view.converged = hst->converged;
+  T->view.iterations = hst->converged ? hst->iterations : hst->j;
+  if (hst->failure == RCG_FAIL_WAW) T->view.iterations = hst->j;
+  T->view.n_betas = hst->converged ? T->view.iterations - 1 : hst->j;
+  finish_view();
+  *trace_out = T;
+  if (hst->failure) {
+    return set_error(c, RCG_ERR_NUMERICAL, "%s",
+                     hst->failure == RCG_FAIL_RZ ? "(r, z) <= 0: preconditioner or operator not SPD"
+                                                 : "(w, A w) <= 0: operator not SPD on search space");
+  }
+  return RCG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// deflation build / project / initial guess (solver.py:63-117)
+
+extern "C" int rcg_deflation_build(rcg_ctx* ctx, const rcg_csr* A, const double* C, int64_t ldc, int64_t n_c,
+                                   double* AC, int64_t ldac, double* L, double* Ginv, int64_t* bad_col_host) {
+  if (!ctx || !A) return RCG_ERR_CONTRACT;
+  if (bad_col_host) *bad_col_host = -1;
+  if (n_c == 0) return RCG_OK;
+  Ctx* c = ctx;
+  int rc = rcg_spmm(ctx, A, C, ldc, n_c, AC, ldac);          // AC = A C
+  if (rc) return rc;
+  double* G = nullptr;
+  RCG_CUDA(c, cudaMallocAsync((void**)&G, sizeof(double) * (size_t)n_c * n_c, c->stream));
+  rc = gemm_tn(c, A->n, n_c, n_c, C, ldc, AC, ldac, G, 1);   // 0.5 (C^T AC + (C^T AC)^T)
+  if (!rc) {
+    int64_t bad = -1;
+    rc = cholesky(c, G, n_c, 1e-12, L, Ginv, &bad);        // pivot_rtol=1e-12 (solver.py:116)
+    if (bad_col_host) *bad_col_host = bad;
+  }
+  cudaFreeAsync(G, c->stream);
+  if (!rc) RCG_CUDA(c, cudaStreamSynchronize(c->stream));
+  return rc;
+}
+
+extern "C" int rcg_project(rcg_ctx* ctx, const rcg_deflation* D, const double* x, double* out) {
+  if (!ctx || !D) return RCG_ERR_CONTRACT;
+  Ctx* c = ctx;
+  if (D->n_c == 0) {
+    RCG_CUDA(c, cudaMemcpyAsync(out, x, sizeof(double) * D->n, cudaMemcpyDeviceToDevice, c->stream));
+    return RCG_OK;
+  }
+  double* u = nullptr;
+  RCG_CUDA(c, cudaMallocAsync((void**)&u, sizeof(double) * (size_t)D->n_c, c->stream));
+  int rc = gemv_t(c, D->n, D->n_c, D->AC, D->ldac, x, u);   // AC^T x
+  if (!rc) rc = coarse_combine(c, D, u, x, out);            // x - C G^{-1} AC^T x
+  cudaFreeAsync(u, c->stream);
+  return rc;
+}
+
+extern "C" int rcg_initial_guess(rcg_ctx* ctx, const rcg_deflation* D, const double* b, double* x0) {
+  if (!ctx || !D) return RCG_ERR_CONTRACT;
+  Ctx* c = ctx;
+  if (D->n_c == 0) {
+    RCG_CUDA(c, cudaMemsetAsync(x0, 0, sizeof(double) * D->n, c->stream));
+    return RCG_OK;
+  }
+  double* u = nullptr;
+  RCG_CUDA(c, cudaMallocAsync((void**)&u, sizeof(double) * (size_t)D->n_c, c->stream));
+  int rc = gemv_t(c, D->n, D->n_c, D->C, D->ldc, b, u);     // C^T b
+  if (!rc) rc = coarse_combine(c, D, u, nullptr, x0);       // C G^{-1} C^T b
+  cudaFreeAsync(u, c->stream);
+  return rc;
+}

@@ -1,0 +1,163 @@
+// Internal helpers shared by the rcg CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <cstdio>
+#include <cstdarg>
+
+#include "../../include/rcg.h"
+
+namespace rcg {
+
+constexpr int kThreads = 256;           // default CTA size for streaming kernels
+constexpr int kWarps = kThreads / 32;
+
+// ---------------------------------------------------------------------------
+// context
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  size_t smem_optin = 227 * 1024;
+  std::string err;
+  int64_t launches = 0;
+  // generic scratch (grown on demand; stream-ordered)
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  unsigned int* counters = nullptr;     // zero-initialised last-block counters
+  int n_counters = 64;
+  double* pinned = nullptr;             // small pinned host staging buffer
+};
+
+int set_error(Ctx* c, int code, const char* fmt, ...);
+
+#define RCG_CUDA(ctx, call)                                                   \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess)                                                    \
+      return ::rcg::set_error((ctx), RCG_ERR_CUDA, "%s: %s (%s:%d)", #call,   \
+                              cudaGetErrorString(e_), __FILE__, __LINE__);    \
+  } while (0)
+
+#define RCG_LAUNCH_CHECK(ctx)                                                 \
+  do {                                                                        \
+    (ctx)->launches++;                                                        \
+    cudaError_t e_ = cudaGetLastError();                                      \
+    if (e_ != cudaSuccess)                                                    \
+      return ::rcg::set_error((ctx), RCG_ERR_CUDA, "launch: %s (%s:%d)",      \
+                              cudaGetErrorString(e_), __FILE__, __LINE__);    \
+  } while (0)
+
+// scratch of at least `bytes` (device, 256-B aligned); invalidates earlier pointers
+int scratch(Ctx* c, size_t bytes, void** out);
+
+// ---------------------------------------------------------------------------
+// device helpers
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Fixed-order block sum; result valid in thread 0 (and returned to all via smem).
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sm /* >= NT/32 */) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sm[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (wid == 0) {
+    t = lane < NT / 32 ? sm[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) sm[0] = t;
+  }
+  __syncthreads();
+  t = sm[0];
+  __syncthreads();
+  return t;
+}
+
+// Last-block-done: every block has written its K partials to part[blockIdx*K+k];
+// returns true in exactly one block (the last to arrive), after which that
+// block may read all partials.  The counter is reset by the last block.
+__device__ __forceinline__ bool arrive_last(unsigned int* counter) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int prev = atomicAdd(counter, 1u);
+    last = (prev == gridDim.x - 1);
+    if (last) *counter = 0u;
+  }
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
+// Deterministic reduction of part[b*K + k] over b < nb for k < K into out[k]
+// by one block of NT threads: warps own k's; lanes stride over blocks in a
+// fixed order then a fixed shuffle tree.
+template <int NT>
+__device__ void reduce_partials(const double* part, int nb, int K, double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int k = wid; k < K; k += NT / 32) {
+    double s = 0.0;
+    for (int b = lane; b < nb; b += 32) s += __ldcg(part + (size_t)b * K + k);
+    s = warp_sum(s);
+    if (lane == 0) out[k] = s;
+  }
+}
+
+__host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ __forceinline__ int64_t pad_ld(int64_t n) { return ceil_div(n, 32) * 32; }
+
+// A column of a column-major history buffer chosen by the device-side
+// iteration counter: column (j + shift) (mod `mod` when mod > 0).
+struct ColSel {
+  double* base;
+  int64_t ld;
+  int64_t mod;
+  int64_t shift;
+  __device__ __forceinline__ double* at(long long j) const {
+    long long c = j + shift;
+    if (mod > 0) c %= mod;
+    return base + (int64_t)c * ld;
+  }
+};
+
+__host__ __forceinline__ ColSel colsel(double* base, int64_t ld = 0, int64_t mod = 1, int64_t shift = 0) {
+  ColSel s;
+  s.base = base;
+  s.ld = ld;
+  s.mod = mod;
+  s.shift = shift;
+  return s;
+}
+
+// Device-resident solve state (one per apcg_solve), read by every kernel of
+// the iteration so that a batch of iterations can be queued (or graph-
+// replayed) with identical launch parameters and no host round trip.
+struct SolveState {
+  long long j;          // index of the current direction w_j
+  long long iterations; // m so far
+  int done;             // converged / failed: every later kernel is a no-op
+  int converged;
+  int failure;          // rcg_failure
+  int pad;
+  double rz;            // (r_j, z_j)
+  double tol_abs;       // tol * ||r0||
+};
+
+// row-offset load for int32/int64 CSR
+template <typename RO>
+__device__ __forceinline__ int64_t ro_at(const RO* ro, int64_t i) { return (int64_t)__ldg(ro + i); }
+
+}  // namespace rcg
+
+struct rcg_ctx : public rcg::Ctx {};

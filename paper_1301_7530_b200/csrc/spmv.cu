@@ -1,0 +1,228 @@
+// fp64 CSR SpMV for sm_100a, with fused dot-product epilogues.
+//
+// Replaces scipy's csr_matvec behind SparseSpdMatrix.__matmul__
+// (/root/reference/pkg/src/recycg/core.py:110-111) at the call sites
+// solver.py:213 (r0 = b - A x0) and solver.py:242-243 (Aw and (w, Aw)).
+//
+// Mapping: a group of V lanes per row (V = 1 for 5/7-point stencils, 8..32 for
+// ~80 nnz/row Q1 elasticity); a warp walks 32/V consecutive rows per step so
+// values / column indices stream coalesced and all lanes execute the shuffles.
+// Epilogue modes (fused so the vector is not re-read):
+//   MODE 0: y = A x
+//   MODE 1: y = A x,      partial (x, y)                 -> out[0]
+//   MODE 2: y = b - A x,  partials (y, y), (b, b)        -> out[0], out[1]
+// Block partials are reduced by the last block in a fixed order.
+#include "rcg_internal.cuh"
+#include "spmv.cuh"
+
+namespace rcg {
+
+template <typename RO, int V, int MODE>
+__global__ void __launch_bounds__(kThreads)
+spmv_kernel(int64_t n, const RO* __restrict__ ro, const int32_t* __restrict__ ci,
+            const double* __restrict__ va, ColSel xs, ColSel ys, const double* __restrict__ b,
+            const SolveState* st, double* part, unsigned int* counter, double* out) {
+  long long j = 0;
+  if (st) {
+    if (st->done) return;
+    j = st->j;
+  }
+  const double* __restrict__ x = xs.at(j);
+  double* __restrict__ y = ys.at(j);
+  constexpr int RPW = 32 / V;                 // rows per warp step
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % V;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int64_t r0 = warp * RPW; r0 < n; r0 += nwarps * RPW) {
+    const int64_t row = r0 + lane / V;
+    double s = 0.0;
+    if (row < n) {
+      const int64_t rs = ro_at(ro, row), re = ro_at(ro, row + 1);
+      int64_t k = rs + sub;
+      // two independent accumulators for memory-level parallelism
+      double s1 = 0.0;
+      for (; k + V < re; k += 2 * V) {
+        s += __ldg(va + k) * __ldg(x + __ldg(ci + k));
+        s1 += __ldg(va + k + V) * __ldg(x + __ldg(ci + k + V));
+      }
+      if (k < re) s += __ldg(va + k) * __ldg(x + __ldg(ci + k));
+      s += s1;
+    }
+#pragma unroll
+    for (int o = V / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (row < n && sub == 0) {
+      double yv;
+      if (MODE == 2) {
+        const double bv = b[row];
+        yv = bv - s;
+        acc1 += bv * bv;
+        acc0 += yv * yv;
+      } else {
+        yv = s;
+        if (MODE == 1) acc0 += x[row] * yv;
+      }
+      y[row] = yv;
+    }
+  }
+  if (MODE == 0) return;
+  __shared__ double sm[kWarps];
+  const double t0 = block_sum<kThreads>(acc0, sm);
+  double t1 = 0.0;
+  if (MODE == 2) t1 = block_sum<kThreads>(acc1, sm);
+  constexpr int K = MODE == 2 ? 2 : 1;
+  if (threadIdx.x == 0) {
+    part[(size_t)blockIdx.x * K] = t0;
+    if (K == 2) part[(size_t)blockIdx.x * K + 1] = t1;
+  }
+  if (arrive_last(counter)) reduce_partials<kThreads>(part, gridDim.x, K, out);
+}
+
+int spmv_width(const rcg_csr* A) {
+  const double avg = A->n > 0 ? (double)A->nnz / (double)A->n : 0.0;
+  if (avg <= 8.0) return 1;
+  if (avg <= 16.0) return 4;
+  if (avg <= 40.0) return 8;
+  if (avg <= 96.0) return 16;
+  return 32;
+}
+
+int spmv_grid(Ctx* c, const rcg_csr* A, int V) {
+  // enough warps to cover the rows once, capped at 8 CTAs/SM resident
+  const int64_t rows_per_cta = (int64_t)(kThreads / 32) * (32 / V);
+  int64_t g = ceil_div(A->n, rows_per_cta);
+  const int64_t cap = (int64_t)c->num_sms * 8;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+template <typename RO, int MODE>
+static void launch_v(int V, int grid, cudaStream_t s, const rcg_csr* A, ColSel xs, ColSel ys,
+                     const double* b, const SolveState* st, double* part, unsigned* cnt, double* out) {
+  const RO* ro = (const RO*)A->row_offsets;
+#define RCG_SPMV_CASE(VV)                                                                  \
+  case VV:                                                                                 \
+    spmv_kernel<RO, VV, MODE><<<grid, kThreads, 0, s>>>(A->n, ro, A->col_indices, A->values, \
+                                                         xs, ys, b, st, part, cnt, out);   \
+    break;
+  switch (V) {
+    RCG_SPMV_CASE(1)
+    RCG_SPMV_CASE(2)
+    RCG_SPMV_CASE(4)
+    RCG_SPMV_CASE(8)
+    RCG_SPMV_CASE(16)
+    default:
+      spmv_kernel<RO, 32, MODE><<<grid, kThreads, 0, s>>>(A->n, ro, A->col_indices, A->values,
+                                                           xs, ys, b, st, part, cnt, out);
+  }
+#undef RCG_SPMV_CASE
+}
+
+int launch_spmv(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const double* b,
+                const SolveState* st, double* part, unsigned int* counter, double* out) {
+  const int V = spmv_width(A);
+  const int grid = spmv_grid(c, A, V);
+  if (A->row_offsets_64) {
+    if (mode == 0) launch_v<int64_t, 0>(V, grid, c->stream, A, xs, ys, b, st, part, counter, out);
+    else if (mode == 1) launch_v<int64_t, 1>(V, grid, c->stream, A, xs, ys, b, st, part, counter, out);
+    else launch_v<int64_t, 2>(V, grid, c->stream, A, xs, ys, b, st, part, counter, out);
+  } else {
+    if (mode == 0) launch_v<int32_t, 0>(V, grid, c->stream, A, xs, ys, b, st, part, counter, out);
+    else if (mode == 1) launch_v<int32_t, 1>(V, grid, c->stream, A, xs, ys, b, st, part, counter, out);
+    else launch_v<int32_t, 2>(V, grid, c->stream, A, xs, ys, b, st, part, counter, out);
+  }
+  RCG_LAUNCH_CHECK(c);
+  return RCG_OK;
+}
+
+int spmv_partials(Ctx* c, const rcg_csr* A) { return spmv_grid(c, A, spmv_width(A)); }
+
+// ---------------------------------------------------------------------------
+// diagonal extraction (core.py:103-104) and Jacobi inverse (solver.py:39-41)
+
+template <typename RO>
+__global__ void diag_kernel(int64_t n, const RO* __restrict__ ro, const int32_t* __restrict__ ci,
+                            const double* __restrict__ va, double* diag, double* inv, int* missing) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rs = ro_at(ro, i), re = ro_at(ro, i + 1);
+    double d = 0.0;
+    bool found = false;
+    for (int64_t k = rs; k < re; ++k)
+      if (ci[k] == i) {
+        d = va[k];
+        found = true;
+        break;
+      }
+    if (!found) atomicExch(missing, 1);
+    if (diag) diag[i] = d;
+    if (inv) inv[i] = 1.0 / d;
+  }
+}
+
+__global__ void diag_apply_kernel(int64_t n, const double* __restrict__ inv, const double* __restrict__ x,
+                                  double* __restrict__ y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = inv ? inv[i] * x[i] : x[i];
+}
+
+int elementwise_grid(Ctx* c, int64_t n) {
+  int64_t g = ceil_div(n, kThreads);
+  const int64_t cap = (int64_t)c->num_sms * 8;
+  return (int)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+}  // namespace rcg
+
+using namespace rcg;
+
+extern "C" int rcg_spmv(rcg_ctx* ctx, const rcg_csr* A, const double* x, double* y) {
+  if (!ctx || !A) return RCG_ERR_CONTRACT;
+  if (A->n == 0) return RCG_OK;
+  return launch_spmv(ctx, A, 0, colsel((double*)x), colsel(y), nullptr, nullptr, nullptr, nullptr,
+                     nullptr);
+}
+
+extern "C" int rcg_spmm(rcg_ctx* ctx, const rcg_csr* A, const double* X, int64_t ldx, int64_t k,
+                        double* Y, int64_t ldy) {
+  if (!ctx || !A || ldx < A->n || ldy < A->n) return ctx ? set_error(ctx, RCG_ERR_CONTRACT, "rcg_spmm: bad ld") : RCG_ERR_CONTRACT;
+  for (int64_t c = 0; c < k; ++c) {
+    int rc = launch_spmv(ctx, A, 0, colsel((double*)X + c * ldx), colsel(Y + c * ldy), nullptr, nullptr,
+                         nullptr, nullptr, nullptr);
+    if (rc) return rc;
+  }
+  return RCG_OK;
+}
+
+extern "C" int rcg_csr_diagonal(rcg_ctx* ctx, const rcg_csr* A, double* diag, double* inv_diag) {
+  if (!ctx || !A) return RCG_ERR_CONTRACT;
+  if (A->n == 0) return RCG_OK;
+  int* missing = nullptr;
+  int rc = scratch(ctx, 256, (void**)&missing);
+  if (rc) return rc;
+  RCG_CUDA(ctx, cudaMemsetAsync(missing, 0, sizeof(int), ctx->stream));
+  const int g = elementwise_grid(ctx, A->n);
+  if (A->row_offsets_64)
+    diag_kernel<int64_t><<<g, kThreads, 0, ctx->stream>>>(A->n, (const int64_t*)A->row_offsets,
+                                                          A->col_indices, A->values, diag, inv_diag, missing);
+  else
+    diag_kernel<int32_t><<<g, kThreads, 0, ctx->stream>>>(A->n, (const int32_t*)A->row_offsets,
+                                                          A->col_indices, A->values, diag, inv_diag, missing);
+  RCG_LAUNCH_CHECK(ctx);
+  int h = 0;
+  RCG_CUDA(ctx, cudaMemcpyAsync(&h, missing, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  RCG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (h) return set_error(ctx, RCG_ERR_CONTRACT, "all diagonal entries must be present and positive");
+  return RCG_OK;
+}
+
+extern "C" int rcg_diag_apply(rcg_ctx* ctx, int64_t n, const double* inv_diag, const double* x, double* y) {
+  if (!ctx) return RCG_ERR_CONTRACT;
+  if (n == 0) return RCG_OK;
+  diag_apply_kernel<<<elementwise_grid(ctx, n), kThreads, 0, ctx->stream>>>(n, inv_diag, x, y);
+  RCG_LAUNCH_CHECK(ctx);
+  return RCG_OK;
+}

@@ -1,0 +1,10 @@
+#pragma once
+#include "rcg_internal.cuh"
+
+namespace rcg {
+// mode 0: y = A x; 1: y = A x + (x,y) -> out[0]; 2: y = b - A x + (y,y),(b,b) -> out[0..1]
+int launch_spmv(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const double* b,
+                const SolveState* st, double* part, unsigned int* counter, double* out);
+int spmv_partials(Ctx* c, const rcg_csr* A);  // number of partial slots per value
+int elementwise_grid(Ctx* c, int64_t n);
+}  // namespace rcg

@@ -1,0 +1,202 @@
+"""Generate golden vectors by running the REFERENCE package (read-only import).
+
+Run in the build container only (``/root/reference`` does not exist on the GPU
+box):  ``python tests/golden/make_golden.py``.  Inputs come from this repo's
+seeded generators (same host CSR bytes the GPU path consumes); their sha256 is
+stored so the tests can prove the generator still emits the bytes the reference
+was run on.  Outputs: ``tests/golden/*.npz`` / ``*.json``.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+REPO = HERE.parents[1]
+sys.path.insert(0, str(REPO))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import recycg  # noqa: E402  (the reference)
+from recycg import recycle as ref_recycle  # noqa: E402
+from recycg import problems as ref_problems  # noqa: E402
+
+from paper_1301_7530_b200 import problems  # noqa: E402
+
+
+def csr_sha(A):
+    h = hashlib.sha256()
+    h.update(np.asarray(A.row_offsets, dtype=np.int64).tobytes())
+    h.update(np.asarray(A.col_indices, dtype=np.int64).tobytes())
+    h.update(np.asarray(A.values, dtype=np.float64).tobytes())
+    return h.hexdigest()
+
+
+def to_ref(A):
+    return recycg.SparseSpdMatrix(A.n, np.asarray(A.row_offsets), np.asarray(A.col_indices),
+                                  np.asarray(A.values))
+
+
+def small_solve_cases():
+    """Dense random SPD cases (reference conftest random_spd), C random, both
+    preconditioners, reorth on/off, plus a cap-stopped run."""
+    rng = np.random.Generator(np.random.Philox(2024))
+    cases = {}
+    specs = [
+        # name, n, n_c, cond, precond, reorth, tol, max_iters, store
+        ("id_noC", 40, 0, 1e3, "identity", True, 1e-10, 500, False),
+        ("jac_C4", 60, 4, 1e4, "jacobi", True, 1e-10, 500, True),
+        ("jac_C6_noreorth", 80, 6, 1e4, "jacobi", False, 1e-10, 500, False),
+        ("user_C3", 50, 3, 1e3, "user", True, 1e-9, 500, False),
+        ("cap_stop", 90, 2, 1e6, "jacobi", True, 1e-14, 7, True),
+        ("big_C40", 120, 40, 1e4, "jacobi", True, 1e-10, 500, False),
+    ]
+    for name, n, n_c, cond, pc, reorth, tol, mi, store in specs:
+        G = problems.random_spd(n, rng, cond)
+        # a non-constant diagonal makes Jacobi matter
+        s = rng.uniform(0.5, 2.0, n)
+        G = G * np.outer(s, s)
+        G = 0.5 * (G + G.T)
+        A = recycg.SparseSpdMatrix.from_dense(G, keep_zeros=True)
+        C = rng.standard_normal((n, n_c))
+        b = rng.standard_normal(n)
+        ud = rng.uniform(0.5, 4.0, n)
+        if pc == "identity":
+            M = recycg.Preconditioner.identity()
+        elif pc == "jacobi":
+            M = recycg.Preconditioner.jacobi(A)
+        else:
+            M = recycg.Preconditioner.user_diagonal(ud)
+        D = recycg.build_deflation(A, C)
+        cfg = recycg.SolveConfig(tol=tol, max_iters=mi, reorthogonalize=reorth,
+                                 trace_capture=True, store_directions=store)
+        x, tr = recycg.apcg_solve(A, M, D, b, cfg)
+        d = dict(dense=A.to_dense(), C=C, b=b, user_diag=ud, precond=pc,
+                 reorth=reorth, tol=tol, max_iters=mi, store=store,
+                 x=x, alphas=np.array(tr.alphas), betas=np.array(tr.betas),
+                 rz=np.array(tr.rz_inner), rnorms=np.array(tr.residual_norms),
+                 iterations=tr.iterations, converged=tr.converged,
+                 L=D.coarse_factor, AC=D.ac)
+        if tr.iterations >= 2:
+            spec = ref_recycle.select_spectrum(tr, recycg.RecycleStrategy("srks", epsilon=1e-10))
+            d["ritz_values"] = spec.values
+            d["ritz_mask"] = spec.converged_mask
+            view = recycg.lanczos_from_trace(tr)
+            d["ritz_prev"] = recycg.tridiag_eig(view.tridiag.truncated(view.m - 1)).values
+            idx = np.flatnonzero(spec.converged_mask)
+            d["ritz_block"] = spec.vectors[:, idx] / np.sqrt(np.abs(spec.values[idx]))
+        cases[name] = d
+    out = {}
+    for name, d in cases.items():
+        for k, v in d.items():
+            out[f"{name}__{k}"] = np.asarray(v)
+    np.savez_compressed(HERE / "small_solves.npz", names=np.array(list(cases)), **out)
+    print("small_solves:", {k: int(v["iterations"]) for k, v in cases.items()})
+
+
+def config1_sequence():
+    """BASELINE config 1 through the reference run_sequence: SRKS eps=1e-10,
+    nc_limit 21, tol 1e-8, Jacobi, reorth on."""
+    systems = problems.shifted_laplacian_sequence()
+    # the base operator must be byte-identical to the reference's own assembler
+    A0_ref = ref_problems._assemble_diffusion(np.ones((128, 128)))
+    A0 = problems.assemble_diffusion(np.ones((128, 128)))
+    assert csr_sha(A0_ref) == csr_sha(A0), "diffusion assembler drifted from reference"
+    shas = [csr_sha(A) for A, _ in systems]
+    bsha = [hashlib.sha256(b.tobytes()).hexdigest() for _, b in systems]
+    ref_systems = [(to_ref(A), b) for A, b in systems]
+    cfg = recycg.SolveConfig(tol=1e-8, max_iters=2000)
+    rep = recycg.run_sequence(iter(ref_systems), recycg.Preconditioner.jacobi,
+                              recycg.RecycleStrategy("srks", epsilon=1e-10, nc_limit=21), cfg)
+    sel_vals = [[float(t[2]) for t in rep.final_tags]]  # final basis provenance
+    # per-system selected Ritz values via the tags the reference records
+    # (re-run with per-step capture for values of every step)
+    per_step = []
+    state = ref_recycle.AugmentationState.from_initial(systems[0][0].n)
+    xs = []
+    for k, (A, b) in enumerate(ref_systems):
+        D = ref_recycle.guarded_deflation(A, state, [])
+        x, tr = recycg.apcg_solve(A, recycg.Preconditioner.jacobi(A), D, b,
+                                  recycg.SolveConfig(tol=1e-8, max_iters=2000))
+        spec = ref_recycle.select_spectrum(tr, recycg.RecycleStrategy("srks", epsilon=1e-10))
+        idx = np.flatnonzero(spec.converged_mask)
+        per_step.append([float(v) for v in spec.values[idx]])
+        ref_recycle.update_basis_srks(state, spec, k)
+        if state.n_c >= 21:
+            state.restart()
+        xs.append(x)
+    data = dict(
+        matrix_sha256=shas, rhs_sha256=bsha,
+        iterations=rep.iterations(), n_c_before=rep.n_c_history(),
+        n_c_selected=[r.n_c_selected for r in rep.records],
+        final_residual=[r.final_residual for r in rep.records],
+        converged=[bool(r.converged) for r in rep.records],
+        events=[list(map(str, e)) for e in rep.events],
+        selected_ritz_values=per_step,
+        final_tags=sel_vals,
+    )
+    (HERE / "config1_sequence.json").write_text(json.dumps(data, indent=1) + "\n")
+    np.savez_compressed(HERE / "config1_solutions.npz", x0=xs[0], x1=xs[1], x9=xs[-1])
+    print("config1 iterations:", data["iterations"], "n_c:", data["n_c_before"])
+
+
+def benchmark_srks():
+    """Reference benchmark (problems.py:89-96), first 8 systems, SRKS eps=1e-10
+    at tol 1e-6 (bit-stable per SURVEY.md §0 finding 2), plus generator pin."""
+    spec_ref = ref_problems.benchmark_spec(seed=0)
+    ref_systems = list(ref_problems.generate_diffusion_sequence(spec_ref, 8))
+    mine = list(problems.generate_diffusion_sequence(problems.benchmark_spec(seed=0), 8))
+    for (Ar, br), (Am, bm) in zip(ref_systems, mine):
+        assert csr_sha(Ar) == csr_sha(Am) and np.array_equal(br, bm), "benchmark generator drifted"
+    cfg = recycg.SolveConfig(tol=1e-6, max_iters=3000)
+    out = {"matrix_sha256": [csr_sha(A) for A, _ in mine]}
+    for name, strat in [("srks10", recycg.RecycleStrategy("srks", epsilon=1e-10)),
+                        ("srks6", recycg.RecycleStrategy("srks", epsilon=1e-6)),
+                        ("clust10", recycg.RecycleStrategy("srks_cluster", epsilon=1e-10))]:
+        rep = recycg.run_sequence(iter(ref_systems), recycg.Preconditioner.jacobi, strat, cfg)
+        out[name] = dict(iterations=rep.iterations(), n_c_before=rep.n_c_history(),
+                         events=[list(map(str, e)) for e in rep.events])
+        print(name, rep.iterations(), rep.n_c_history())
+    (HERE / "benchmark_srks.json").write_text(json.dumps(out, indent=1) + "\n")
+
+
+def elasticity_small():
+    """Config-2 analog at 8^3 elements (n = 8*9*9*3 = 1944): 4 RHS SRKS."""
+    systems = list(problems.elasticity_sequence(8, 4, kind="fixed"))
+    A = systems[0][0]
+    Ar = recycg.SparseSpdMatrix(A.n, A.row_offsets, A.col_indices, A.values)  # validates symmetry
+    cfg = recycg.SolveConfig(tol=1e-8, max_iters=3000)
+    rep = recycg.run_sequence(iter([(Ar, b) for _, b in systems]), recycg.Preconditioner.jacobi,
+                              recycg.RecycleStrategy("srks", epsilon=1e-10, nc_limit=61), cfg)
+    out = dict(matrix_sha256=csr_sha(A), iterations=rep.iterations(),
+               n_c_before=rep.n_c_history(),
+               final_residual=[r.final_residual for r in rep.records])
+    (HERE / "elasticity8_sequence.json").write_text(json.dumps(out, indent=1) + "\n")
+    print("elasticity8", rep.iterations(), rep.n_c_history())
+
+
+def pilot_fixture():
+    """Copy of the reference's frozen golden lists that reproduce exactly
+    (none/trks; SURVEY.md §0 finding 2): pkg/tests/fixtures/benchmark_pilot.json."""
+    src = json.loads(Path("/root/reference/pkg/tests/fixtures/benchmark_pilot.json").read_text())
+    keep = {"source": "reference pkg/tests/fixtures/benchmark_pilot.json (none, trks lists)",
+            "runs": {tol: {s: src["runs"][tol][s] for s in ("none", "trks") if s in src["runs"][tol]}
+                     for tol in src["runs"]}}
+    (HERE / "benchmark_pilot_none_trks.json").write_text(json.dumps(keep, indent=1) + "\n")
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["small", "config1", "bench", "elast", "pilot"]
+    if "pilot" in which:
+        pilot_fixture()
+    if "small" in which:
+        small_solve_cases()
+    if "elast" in which:
+        elasticity_small()
+    if "bench" in which:
+        benchmark_srks()
+    if "config1" in which:
+        config1_sequence()

@@ -1,0 +1,152 @@
+"""GPU parity of the individual kernels against the CPU oracle / closed forms."""
+import numpy as np
+import pytest
+import scipy.linalg
+
+import paper_1301_7530_b200 as rcg
+from paper_1301_7530_b200 import problems
+from oracle import recycg_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def _spmv_close(A, x):
+    y = rcg.spmv(A, x)
+    want = orc.spmv(A, x)
+    # reduction order differs from scipy: bound by ulps of |A||x| per row
+    absrow = orc.csr(type("M", (), dict(n=A.n, row_offsets=A.row_offsets, col_indices=A.col_indices,
+                                         values=np.abs(A.values)))) @ np.abs(x)
+    assert np.all(np.abs(y - want) <= 8 * np.finfo(float).eps * absrow + 1e-300)
+
+
+def test_spmv_config1_and_stencils(rng):
+    A, _ = problems.shifted_laplacian_sequence(grid=128, count=2)[1]
+    _spmv_close(A, rng.standard_normal(A.n))
+    B = problems.assemble_diffusion(np.exp(rng.standard_normal((12, 10, 9))))
+    _spmv_close(B, rng.standard_normal(B.n))
+
+
+def test_spmv_elasticity_and_dense(rng):
+    E = problems.elasticity_q1(6)
+    _spmv_close(E, rng.standard_normal(E.n))
+    D = rcg.SparseSpdMatrix.from_dense(problems.random_spd(70, rng), keep_zeros=True)
+    _spmv_close(D, rng.standard_normal(70))
+
+
+def test_spmv_kats():
+    # reference tests/test_core.py:71-91
+    A = rcg.SparseSpdMatrix.from_dense(np.eye(3))
+    np.testing.assert_array_equal(rcg.spmv(A, [1.0, 2.0, 3.0]), [1.0, 2.0, 3.0])
+    lap = 2.0 * np.eye(4) - np.eye(4, k=1) - np.eye(4, k=-1)
+    np.testing.assert_array_equal(rcg.spmv(rcg.SparseSpdMatrix.from_dense(lap), [1.0, 0, 0, 0]),
+                                  [2.0, -1.0, 0.0, 0.0])
+    with pytest.raises(rcg.ContractViolation):
+        rcg.spmv(A, np.ones(4))
+
+
+def test_spmm_block(rng):
+    A = problems.assemble_diffusion(np.ones((20, 17)))
+    X = rng.standard_normal((A.n, 5))
+    Y = A @ X
+    np.testing.assert_allclose(Y, orc.csr(A) @ X, rtol=1e-13, atol=1e-13)
+
+
+def test_diagonal_and_jacobi():
+    A = rcg.SparseSpdMatrix.from_dense(np.diag([2.0, 4.0]))
+    M = rcg.Preconditioner.jacobi(A)
+    np.testing.assert_allclose(M.apply(np.array([2.0, 4.0])), [1.0, 1.0])
+    np.testing.assert_allclose(M.diag(), [2.0, 4.0])
+    np.testing.assert_array_equal(A.diagonal(), [2.0, 4.0])
+
+
+@pytest.mark.parametrize("n", [2, 3, 10, 50, 127, 200])
+def test_cholesky_matches_oracle(rng, n):
+    G = problems.random_spd(n, rng)
+    L = rcg.dense_cholesky(G)
+    np.testing.assert_allclose(L, np.linalg.cholesky(G), rtol=1e-10, atol=1e-12)
+
+
+def test_cholesky_kats():
+    np.testing.assert_allclose(rcg.dense_cholesky(np.array([[4.0, 2.0], [2.0, 2.0]])), [[2.0, 0.0], [1.0, 1.0]])
+    with pytest.raises(rcg.RankDeficient) as ei:
+        rcg.dense_cholesky(np.array([[1.0, 1.0], [1.0, 1.0]]))
+    assert ei.value.column == 1
+    with pytest.raises(rcg.ContractViolation):
+        rcg.dense_cholesky(np.array([[1.0, 2.0], [0.0, 1.0]]))
+
+
+@pytest.mark.parametrize("n,bad", [(40, 20), (150, 97)])
+def test_cholesky_rank_deficient_column(rng, n, bad):
+    # reference tests/test_core.py:136-146 (and the > 128 global-memory path)
+    G = problems.random_spd(n, rng)
+    B = np.linalg.cholesky(G)
+    B[:, bad] = B[:, 5] + 2.0 * B[:, 7]
+    G2 = B @ B.T
+    with pytest.raises(rcg.RankDeficient) as ei:
+        rcg.dense_cholesky(0.5 * (G2 + G2.T), pivot_rtol=1e-12)
+    assert ei.value.column == bad
+    with pytest.raises(orc.OracleRankDeficient) as eo:
+        orc.dense_cholesky(0.5 * (G2 + G2.T), pivot_rtol=1e-12)
+    assert eo.value.column == bad
+
+
+def test_tridiag_eig_closed_form():
+    T = rcg.TridiagSym(np.full(4, 2.0), np.full(3, -1.0))
+    eig = rcg.tridiag_eig(T)
+    want = sorted((2.0 - 2.0 * np.cos(k * np.pi / 5.0) for k in range(1, 5)), reverse=True)
+    np.testing.assert_allclose(eig.values, want, rtol=1e-12)
+    H = T.to_dense()
+    for th, q in zip(eig.values, eig.vectors.T):
+        assert np.linalg.norm(H @ q - th * q) <= 1e-10 * np.linalg.norm(H)
+    np.testing.assert_allclose(eig.vectors.T @ eig.vectors, np.eye(4), atol=1e-12)
+
+
+@pytest.mark.parametrize("m", [2, 5, 40, 390, 1200])
+def test_tridiag_eigvals_vs_lapack(rng, m):
+    d = rng.uniform(1.0, 3.0, m)
+    e = rng.uniform(-1.0, 1.0, m - 1)
+    got = rcg.tridiag_eig(rcg.TridiagSym(d, e)) if m <= 400 else None
+    want = orc.tridiag_eigvals(d, e)
+    import torch
+    from paper_1301_7530_b200.core import tridiag_eigvals_device
+    vals = tridiag_eigvals_device(torch.tensor(d, device="cuda"), torch.tensor(e, device="cuda")).cpu().numpy()
+    np.testing.assert_allclose(vals, want, rtol=0, atol=8 * np.finfo(float).eps * np.abs(want).max() * np.sqrt(m))
+    if got is not None:
+        H = rcg.TridiagSym(d, e).to_dense()
+        R = H @ got.vectors - got.vectors * got.values
+        assert np.abs(R).max() <= 1e-10 * np.abs(want).max()
+        np.testing.assert_allclose(got.vectors.T @ got.vectors, np.eye(m), atol=1e-9)
+
+
+def test_select_converged_kats():
+    # reference tests/test_ritz.py:145-182
+    def spec(v):
+        return rcg.RitzSpectrum(np.asarray(v, dtype=float), np.eye(len(v)))
+    assert list(rcg.select_converged(spec([9.0, 5.0, 2.0, 1.0]), [9.0, 5.0, 2.0], 1e-12).converged_mask) == \
+        [True, True, True, False]
+    assert not rcg.select_converged(spec([9.0, 5.0, 2.0]), [9.9, 5.5], 1e-6).converged_mask.any()
+    assert list(rcg.select_converged(spec([9.0, 4.0, 1.0]), [6.0, 1.0], 1e-12).converged_mask) == \
+        [False, False, True]
+    m = rcg.select_converged(spec([5.0, 5.0 * (1 + 1e-15), 1.0]), [5.0, 5.0], 1e-12).converged_mask
+    assert m[0] and not m[1]
+    out = rcg.select_converged(spec([3.0]), [], 1e-6)
+    assert out.m == 1 and not out.converged_mask.any()
+
+
+def test_gemm_tn_nn(rng):
+    import torch
+    from paper_1301_7530_b200 import _lib
+    n, a, b = 1000, 37, 45
+    X = rng.standard_normal((n, a))
+    Y = rng.standard_normal((n, b))
+    Xd = torch.tensor(np.ascontiguousarray(X.T), device="cuda")
+    Yd = torch.tensor(np.ascontiguousarray(Y.T), device="cuda")
+    G = torch.empty((b, a), dtype=torch.float64, device="cuda")
+    ctx = _lib.context()
+    ctx.check(ctx.lib.rcg_gemm_tn(ctx.h, n, a, b, _lib.ptr(Xd), n, _lib.ptr(Yd), n, _lib.ptr(G), 0))
+    np.testing.assert_allclose(G.cpu().numpy().T, X.T @ Y, rtol=1e-12, atol=1e-11)
+    Q = rng.standard_normal((a, 7))
+    Qd = torch.tensor(np.ascontiguousarray(Q.T), device="cuda")
+    Out = torch.empty((7, n), dtype=torch.float64, device="cuda")
+    ctx.check(ctx.lib.rcg_gemm_nn(ctx.h, n, a, 7, _lib.ptr(Xd), n, _lib.ptr(Qd), a, _lib.ptr(Out), n))
+    np.testing.assert_allclose(Out.cpu().numpy().T, X @ Q, rtol=1e-12, atol=1e-11)
