@@ -116,6 +116,27 @@ const char* rcg_last_error(const rcg_ctx* ctx);
 int rcg_version(void);
 int rcg_num_kernel_launches(const rcg_ctx* ctx, int64_t* out_host); /* launches issued by ctx */
 
+/* Live per-kernel-class timing of the solve loop: when enabled, every
+ * iteration kernel is bracketed by CUDA events on the ctx stream and its
+ * ALGORITHMIC bytes (each operand touched once) are accounted.  Classes: */
+enum rcg_kclass {
+  RCG_K_SPMV = 0,      /* K1: Aw = A w, (w, Aw)                         */
+  RCG_K_UPDATE = 1,    /* K2: x, r update, ||r||^2, AC^T y             */
+  RCG_K_COARSE = 2,    /* coarse solve (n_c > 64)                      */
+  RCG_K_PRECOND = 3,   /* K3: z = P M^-1 r, (r, z), AW^T [z w] partials */
+  RCG_K_COLREDUCE = 4, /* K4: reorth partial reduction                  */
+  RCG_K_WUPDATE = 5,   /* K5: w = z + beta w - W c                      */
+  RCG_K_NUM = 6
+};
+typedef struct {
+  int64_t launches;
+  double seconds;
+  double bytes;
+} rcg_kernel_stat;
+int rcg_ctx_set_profiling(rcg_ctx* ctx, int enable);
+int rcg_ctx_kernel_stats(const rcg_ctx* ctx, rcg_kernel_stat* out_host, int n); /* n <= RCG_K_NUM */
+int rcg_ctx_reset_stats(rcg_ctx* ctx);
+
 /* ---- operators (core.py) ------------------------------------------------- */
 /* y = A x  (spmv, core.py:114-119 / SparseSpdMatrix.__matmul__ core.py:110-111) */
 int rcg_spmv(rcg_ctx* ctx, const rcg_csr* A, const double* x, double* y);

@@ -191,7 +191,13 @@ def apcg_solve(A, inv_diag, D, b, tol, max_iters, reorthogonalize=True,
     if rz <= 0.0:
         raise OracleNumericalFailure("(r, z) <= 0: preconditioner or operator not SPD")
     w = z.copy()
-    W, AW, waw = [], [], []
+    # preallocated C-order direction blocks grown geometrically, exactly as the
+    # reference stores them (solver.py:233-240) so BLAS sees the same layout
+    cap = 64
+    W = np.empty((A.n, cap))
+    AW = np.empty((A.n, cap))
+    waw = np.empty(cap)
+    stored = 0
     for _ in range(max_iters):                             # :241-288
         Aw = Acsr @ w
         wAw = float(w @ Aw)
@@ -210,10 +216,16 @@ def apcg_solve(A, inv_diag, D, b, tol, max_iters, reorthogonalize=True,
         rnorm = float(np.linalg.norm(r))
         trace.residual_norms.append(rnorm)
         trace.iterations += 1
-        if reorthogonalize:
-            W.append(w)
-            AW.append(Aw)
-            waw.append(wAw)
+        if reorthogonalize:                                # :262-271
+            if stored == cap:
+                cap *= 2
+                W = np.concatenate([W, np.empty_like(W)], axis=1)
+                AW = np.concatenate([AW, np.empty_like(AW)], axis=1)
+                waw = np.concatenate([waw, np.empty_like(waw)])
+            W[:, stored] = w
+            AW[:, stored] = Aw
+            waw[stored] = wAw
+            stored += 1
         if rnorm <= tol * r0:                              # :273
             trace.converged = True
             break
@@ -225,9 +237,8 @@ def apcg_solve(A, inv_diag, D, b, tol, max_iters, reorthogonalize=True,
         trace.betas.append(beta)
         w = z + beta * w
         if reorthogonalize:                                # :284-287 (block CGS)
-            Wm = np.column_stack(W)
-            AWm = np.column_stack(AW)
-            w = w - Wm @ ((AWm.T @ w) / np.asarray(waw))
+            Wv = W[:, :stored]
+            w = w - Wv @ ((AW[:, :stored].T @ w) / waw[:stored])
         rz = rz_next
     return x, trace
 

@@ -49,6 +49,12 @@ class RcgTraceView(C.Structure):
                 ("device_seconds", C.c_double)]
 
 
+class RcgKernelStat(C.Structure):
+    _fields_ = [("launches", C.c_int64), ("seconds", C.c_double), ("bytes", C.c_double)]
+
+
+KCLASSES = ("spmv", "update", "coarse", "precond", "colreduce", "wupdate")
+
 _vp = C.c_void_p
 _i64 = C.c_int64
 _i32 = C.c_int32
@@ -62,6 +68,9 @@ SIGNATURES = {
     "rcg_last_error": (C.c_char_p, [_vp]),
     "rcg_version": (C.c_int, []),
     "rcg_num_kernel_launches": (C.c_int, [_vp, c_int64_p]),
+    "rcg_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
+    "rcg_ctx_kernel_stats": (C.c_int, [_vp, C.POINTER(RcgKernelStat), C.c_int]),
+    "rcg_ctx_reset_stats": (C.c_int, [_vp]),
     "rcg_spmv": (C.c_int, [_vp, C.POINTER(RcgCsr), _vp, _vp]),
     "rcg_spmm": (C.c_int, [_vp, C.POINTER(RcgCsr), _vp, _i64, _i64, _vp, _i64]),
     "rcg_csr_diagonal": (C.c_int, [_vp, C.POINTER(RcgCsr), _vp, _vp]),
@@ -168,6 +177,18 @@ class Context:
         if rc == RCG_ERR_OOM:
             raise MemoryError(msg or what)
         raise RuntimeError(f"{what}: {msg} (status {rc})")
+
+    def set_profiling(self, on):
+        self.lib.rcg_ctx_set_profiling(self.h, 1 if on else 0)
+
+    def reset_stats(self):
+        self.lib.rcg_ctx_reset_stats(self.h)
+
+    def kernel_stats(self):
+        arr = (RcgKernelStat * len(KCLASSES))()
+        self.lib.rcg_ctx_kernel_stats(self.h, arr, len(KCLASSES))
+        return {k: dict(launches=arr[i].launches, seconds=arr[i].seconds, bytes=arr[i].bytes)
+                for i, k in enumerate(KCLASSES)}
 
     def launches(self):
         v = C.c_int64(0)

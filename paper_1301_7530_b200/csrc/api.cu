@@ -35,9 +35,70 @@ int scratch(Ctx* c, size_t bytes, void** out) {
   return RCG_OK;
 }
 
+static cudaEvent_t pool_get(Ctx* c) {
+  if (!c->event_pool.empty()) {
+    cudaEvent_t e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void prof_begin(Ctx* c, int kclass, double bytes) {
+  if (!c->profiling) return;
+  Ctx::Pending p;
+  p.kclass = kclass;
+  p.bytes = bytes;
+  p.a = pool_get(c);
+  p.b = pool_get(c);
+  cudaEventRecord(p.a, c->stream);
+  c->pending.push_back(p);
+}
+
+void prof_end(Ctx* c) {
+  if (!c->profiling || c->pending.empty()) return;
+  cudaEventRecord(c->pending.back().b, c->stream);
+}
+
+void prof_collect(Ctx* c) {
+  for (auto& p : c->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+      c->stats[p.kclass].launches += 1;
+      c->stats[p.kclass].seconds += ms * 1e-3;
+      c->stats[p.kclass].bytes += p.bytes;
+    } else {
+      cudaGetLastError();
+    }
+    c->event_pool.push_back(p.a);
+    c->event_pool.push_back(p.b);
+  }
+  c->pending.clear();
+}
+
 }  // namespace rcg
 
 using namespace rcg;
+
+extern "C" int rcg_ctx_set_profiling(rcg_ctx* c, int enable) {
+  if (!c) return RCG_ERR_CONTRACT;
+  c->profiling = enable ? 1 : 0;
+  return RCG_OK;
+}
+
+extern "C" int rcg_ctx_kernel_stats(const rcg_ctx* c, rcg_kernel_stat* out, int n) {
+  if (!c || !out) return RCG_ERR_CONTRACT;
+  for (int i = 0; i < n && i < RCG_K_NUM; ++i) out[i] = c->stats[i];
+  return RCG_OK;
+}
+
+extern "C" int rcg_ctx_reset_stats(rcg_ctx* c) {
+  if (!c) return RCG_ERR_CONTRACT;
+  for (int i = 0; i < RCG_K_NUM; ++i) c->stats[i] = rcg_kernel_stat{0, 0.0, 0.0};
+  return RCG_OK;
+}
 
 extern "C" int rcg_version(void) { return 1; }
 
@@ -75,6 +136,11 @@ extern "C" void rcg_ctx_destroy(rcg_ctx* c) {
   if (c->scratch) cudaFree(c->scratch);
   if (c->counters) cudaFree(c->counters);
   if (c->pinned) cudaFreeHost(c->pinned);
+  for (auto& p : c->pending) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : c->event_pool) cudaEventDestroy(e);
   delete c;
 }
 

@@ -64,6 +64,65 @@ struct IterArgs {
   int rows_per_block;
 };
 
+// Tile GEMV-T: partial dots of `ncols` columns (column k at base + k*ld, the
+// tile's first row already applied) with NV smem vectors of length len.
+// Warps own groups of CG consecutive columns, so each vector element loaded
+// from shared memory is reused for CG columns and each lane keeps CG*NV
+// independent accumulators (+ CG loads in flight per row step).
+template <int CG, int NV>
+__device__ __forceinline__ void gemv_t_tile(const double* __restrict__ base, int64_t ld, int64_t ncols, int64_t len,
+                                            const double* __restrict__ v0, const double* __restrict__ v1,
+                                            double* __restrict__ out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t ngroups = (ncols + CG - 1) / CG;
+  for (int64_t g = wid; g < ngroups; g += kWarps) {
+    const int64_t k0 = g * CG;
+    const int kc = (int)min((int64_t)CG, ncols - k0);
+    const double* __restrict__ cols = base + k0 * ld;
+    double a0[CG], a1[CG];
+#pragma unroll
+    for (int c = 0; c < CG; ++c) a0[c] = a1[c] = 0.0;
+    if (kc == CG) {
+#pragma unroll 2
+      for (int64_t i = lane; i < len; i += 32) {
+        const double x0 = v0[i];
+        const double x1 = NV == 2 ? v1[i] : 0.0;
+#pragma unroll
+        for (int c = 0; c < CG; ++c) {
+          const double v = __ldcs(cols + c * ld + i);
+          a0[c] += v * x0;
+          if (NV == 2) a1[c] += v * x1;
+        }
+      }
+    } else {
+      for (int64_t i = lane; i < len; i += 32) {
+        const double x0 = v0[i];
+        const double x1 = NV == 2 ? v1[i] : 0.0;
+#pragma unroll
+        for (int c = 0; c < CG; ++c)
+          if (c < kc) {
+            const double v = __ldcs(cols + c * ld + i);
+            a0[c] += v * x0;
+            if (NV == 2) a1[c] += v * x1;
+          }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < CG; ++c) {
+      a0[c] = warp_sum(a0[c]);
+      if (NV == 2) a1[c] = warp_sum(a1[c]);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < CG; ++c)
+        if (c < kc) {
+          out[(k0 + c) * NV] = a0[c];
+          if (NV == 2) out[(k0 + c) * NV + 1] = a1[c];
+        }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K2: alpha, x/r update, ||r||^2, AC^T y partials.  init != 0: no update
 // (initial residual: only ||r||^2 and AC^T y).
@@ -115,20 +174,7 @@ update_kernel(IterArgs a, int init) {
   if (threadIdx.x == 0) a.part_upd[(size_t)blockIdx.x * K] = rrb;
   if (a.n_c) {
     __syncthreads();
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t len = r1 - r0;
-    for (int64_t c = wid; c < a.n_c; c += kWarps) {
-      const double* col = a.AC + c * a.ldac + r0;
-      double p0 = 0.0, p1 = 0.0;
-      int64_t i = lane;
-      for (; i + 32 < len; i += 64) {
-        p0 += col[i] * ytile[i];
-        p1 += col[i + 32] * ytile[i + 32];
-      }
-      if (i < len) p0 += col[i] * ytile[i];
-      const double p = warp_sum(p0 + p1);
-      if (lane == 0) a.part_upd[(size_t)blockIdx.x * K + 1 + c] = p;
-    }
+    gemv_t_tile<4, 1>(a.AC + r0, a.ldac, a.n_c, r1 - r0, ytile, nullptr, a.part_upd + (size_t)blockIdx.x * K + 1);
   }
   if (arrive_last(a.counters + 1)) reduce_partials<kThreads>(a.part_upd, gridDim.x, (int)K, a.sums + 1);
 }
@@ -216,32 +262,9 @@ precond_kernel(IterArgs a, int init) {
   if (threadIdx.x == 0) a.part_z[blockIdx.x] = rzb;
   if (reo) {
     __syncthreads();
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t len = r1 - r0;
-    double* prow = a.part_reo + (size_t)blockIdx.x * a.reo_stride;
-    for (long long k = wid; k <= j; k += kWarps) {
-      const double* col = a.AW.at(k) + r0;
-      double pz0 = 0.0, pz1 = 0.0, pw0 = 0.0, pw1 = 0.0;
-      int64_t i = lane;
-      for (; i + 32 < len; i += 64) {
-        const double c0 = col[i], c1 = col[i + 32];
-        pz0 += c0 * ztile[i];
-        pw0 += c0 * wtile[i];
-        pz1 += c1 * ztile[i + 32];
-        pw1 += c1 * wtile[i + 32];
-      }
-      if (i < len) {
-        const double c0 = col[i];
-        pz0 += c0 * ztile[i];
-        pw0 += c0 * wtile[i];
-      }
-      const double pz = warp_sum(pz0 + pz1);
-      const double pw = warp_sum(pw0 + pw1);
-      if (lane == 0) {
-        prow[2 * k] = pz;
-        prow[2 * k + 1] = pw;
-      }
-    }
+    // AW is fully stored when reorthogonalizing (mod 0): column k at base + k*ld
+    gemv_t_tile<8, 2>(a.AW.base + r0, a.AW.ld, j + 1, r1 - r0, ztile, wtile,
+                      a.part_reo + (size_t)blockIdx.x * a.reo_stride);
   }
   if (arrive_last(a.counters + 2)) reduce_partials<kThreads>(a.part_z, gridDim.x, 1, a.sums + a.rz_off);
 }
@@ -743,6 +766,9 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
   int64_t it = 0;
   int64_t batch = cfg->batch > 0 ? cfg->batch : 4;
   const int wu_grid = (int)std::max<int64_t>(1, ceil_div(n, (int64_t)kThreads * WU_RPT));
+  const double jac = inv_diag ? 1.0 : 0.0;
+  const double bytes_spmv = 12.0 * (double)A->nnz + (A->row_offsets_64 ? 8.0 : 4.0) * (double)(n + 1) +
+                            16.0 * (double)n;
   bool done = false;
   while (it < max_it && !done) {
     const int64_t B = std::min<int64_t>(batch, max_it - it);
@@ -770,23 +796,40 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
       refresh();
     }
     for (int64_t q = 0; q < B; ++q) {
-      const int64_t jj = it + q;  // upper bound of the device-side j
+      const int64_t jj = it + q;  // the device-side j unless the solve already stopped
+      const double nd = (double)n, js = (double)(jj + 1);
+      // algorithmic bytes per launch (each operand touched once)
+      prof_begin(c, RCG_K_SPMV, bytes_spmv);
       if ((rc = launch_spmv(c, A, 1, a.W, a.AW, nullptr, st, part_spmv, counters + 0, gSum.ptr))) return fail(rc);
+      prof_end(c);
+      prof_begin(c, RCG_K_UPDATE, 8.0 * nd * (6 + jac + n_c + (store ? 1 : 0)));
       update_kernel<<<nb, kThreads, smem_upd, c->stream>>>(a, 0);
       RCG_LAUNCH_CHECK(c);
-      if ((rc = launch_coarse(1))) return fail(rc);
+      prof_end(c);
+      if (n_c > NC_INLINE) {
+        prof_begin(c, RCG_K_COARSE, 8.0 * (double)n_c * (double)n_c);
+        if ((rc = launch_coarse(1))) return fail(rc);
+        prof_end(c);
+      }
+      prof_begin(c, RCG_K_PRECOND, 8.0 * nd * (2 + jac + n_c + (reorth ? 1.0 + js : 0.0)));
       precond_kernel<<<nb, kThreads, smem_pre, c->stream>>>(a, 0);
       RCG_LAUNCH_CHECK(c);
+      prof_end(c);
       if (reorth) {
+        prof_begin(c, RCG_K_COLREDUCE, 8.0 * 2.0 * js * (nb + 1));
         colreduce_kernel<<<(unsigned)ceil_div(2 * (jj + 1), 32), 256, 0, c->stream>>>(a, nb);
         RCG_LAUNCH_CHECK(c);
+        prof_end(c);
       }
+      prof_begin(c, RCG_K_WUPDATE, 8.0 * nd * (3 + (reorth ? js : 0.0)));
       wupdate_kernel<<<wu_grid, kThreads, 0, c->stream>>>(a);
       RCG_LAUNCH_CHECK(c);
+      prof_end(c);
     }
     it += B;
     RCG_CUDA(c, cudaMemcpyAsync(hst, st, sizeof(SolveState), cudaMemcpyDeviceToHost, c->stream));
     RCG_CUDA(c, cudaStreamSynchronize(c->stream));
+    prof_collect(c);
     done = hst->done != 0;
     batch = std::min<int64_t>(batch * 2, 64);
   }

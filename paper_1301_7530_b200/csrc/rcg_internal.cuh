@@ -6,6 +6,7 @@
 #include <string>
 #include <cstdio>
 #include <cstdarg>
+#include <vector>
 
 #include "../../include/rcg.h"
 
@@ -30,7 +31,23 @@ struct Ctx {
   unsigned int* counters = nullptr;     // zero-initialised last-block counters
   int n_counters = 64;
   double* pinned = nullptr;             // small pinned host staging buffer
+  // live kernel timing (rcg_ctx_set_profiling)
+  int profiling = 0;
+  rcg_kernel_stat stats[RCG_K_NUM] = {};
+  struct Pending {
+    int kclass;
+    double bytes;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> event_pool;
 };
+
+// Brackets a launch with events when profiling; `collect` (after a stream
+// sync) folds the elapsed times into the per-class stats.
+void prof_begin(Ctx* c, int kclass, double bytes);
+void prof_end(Ctx* c);
+void prof_collect(Ctx* c);
 
 int set_error(Ctx* c, int code, const char* fmt, ...);
 

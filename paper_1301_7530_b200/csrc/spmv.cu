@@ -15,6 +15,8 @@
 #include "rcg_internal.cuh"
 #include "spmv.cuh"
 
+#include <cstdlib>
+
 namespace rcg {
 
 template <typename RO, int V, int MODE>
@@ -41,14 +43,18 @@ spmv_kernel(int64_t n, const RO* __restrict__ ro, const int32_t* __restrict__ ci
     if (row < n) {
       const int64_t rs = ro_at(ro, row), re = ro_at(ro, row + 1);
       int64_t k = rs + sub;
-      // two independent accumulators for memory-level parallelism
-      double s1 = 0.0;
-      for (; k + V < re; k += 2 * V) {
-        s += __ldg(va + k) * __ldg(x + __ldg(ci + k));
-        s1 += __ldg(va + k + V) * __ldg(x + __ldg(ci + k + V));
+      // four independent accumulators for memory-level parallelism
+      double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      for (; k + 3 * V < re; k += 4 * V) {
+        const int c0 = __ldg(ci + k), c1 = __ldg(ci + k + V), c2 = __ldg(ci + k + 2 * V), c3 = __ldg(ci + k + 3 * V);
+        const double v0 = __ldcs(va + k), v1 = __ldcs(va + k + V), v2 = __ldcs(va + k + 2 * V), v3 = __ldcs(va + k + 3 * V);
+        s += v0 * __ldg(x + c0);
+        s1 += v1 * __ldg(x + c1);
+        s2 += v2 * __ldg(x + c2);
+        s3 += v3 * __ldg(x + c3);
       }
-      if (k < re) s += __ldg(va + k) * __ldg(x + __ldg(ci + k));
-      s += s1;
+      for (; k < re; k += V) s += __ldcs(va + k) * __ldg(x + __ldg(ci + k));
+      s += (s1 + s2) + s3;
     }
 #pragma unroll
     for (int o = V / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -80,11 +86,19 @@ spmv_kernel(int64_t n, const RO* __restrict__ ro, const int32_t* __restrict__ ci
 }
 
 int spmv_width(const rcg_csr* A) {
+  static int forced = -1;
+  if (forced < 0) {
+    const char* e = getenv("RCG_SPMV_V");
+    forced = e ? atoi(e) : 0;
+  }
+  if (forced == 1 || forced == 2 || forced == 4 || forced == 8 || forced == 16 || forced == 32) return forced;
   const double avg = A->n > 0 ? (double)A->nnz / (double)A->n : 0.0;
-  if (avg <= 8.0) return 1;
-  if (avg <= 16.0) return 4;
-  if (avg <= 40.0) return 8;
-  if (avg <= 96.0) return 16;
+  // measured on B200 (tools/spmv_bench.py): 7-pt 256^3 best at V=1,
+  // Q1 elasticity (78.5/row) best at V=4..8
+  if (avg <= 10.0) return 1;
+  if (avg <= 20.0) return 4;
+  if (avg <= 160.0) return 8;
+  if (avg <= 320.0) return 16;
   return 32;
 }
 

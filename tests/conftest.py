@@ -30,6 +30,18 @@ def pytest_collection_modifyitems(config, items):
             item.add_marker(skip)
 
 
+@pytest.fixture(autouse=True, scope="session")
+def _single_thread_blas():
+    # the oracle's GEMVs are tiny; thread fan-out only burns CPU (selection at
+    # eps >= 1e-10 is thread-count stable, SURVEY.md §0 finding 2)
+    try:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=1, user_api="blas"):
+            yield
+    except ImportError:  # pragma: no cover
+        yield
+
+
 @pytest.fixture
 def rng():
     # reference tests/conftest.py:21-23

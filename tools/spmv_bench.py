@@ -1,0 +1,35 @@
+"""Time rcg_spmv on a BASELINE matrix (CUDA events, L2 flushed by the matrix size).
+usage: RCG_SPMV_V=8 python tools/spmv_bench.py [elast64|diff256|lap128]"""
+import sys, time
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np
+import torch
+from paper_1301_7530_b200 import problems, _lib
+
+which = sys.argv[1] if len(sys.argv) > 1 else "elast64"
+if which == "elast64":
+    A = problems.elasticity_q1(64, validate=False)
+elif which == "diff256":
+    A = next(problems.lognormal_diffusion_sequence(256, 1))[0]
+else:
+    A = problems.shifted_laplacian_sequence(count=1)[0][0]
+h = A.device_csr()
+ctx = _lib.context()
+x = torch.randn(A.n, dtype=torch.float64, device="cuda")
+y = torch.empty_like(x)
+for _ in range(5):
+    ctx.check(ctx.lib.rcg_spmv(ctx.h, _lib.C.byref(h.struct), _lib.ptr(x), _lib.ptr(y)))
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+N = 50
+e0.record()
+for _ in range(N):
+    ctx.check(ctx.lib.rcg_spmv(ctx.h, _lib.C.byref(h.struct), _lib.ptr(x), _lib.ptr(y)))
+e1.record()
+torch.cuda.synchronize()
+t = e0.elapsed_time(e1) / N * 1e-3
+byt = 12 * A.nnz + 4 * (A.n + 1) + 16 * A.n
+import os
+print(f"{which} V={os.environ.get('RCG_SPMV_V','auto')} n={A.n} nnz={A.nnz} t={t*1e6:.1f}us  {byt/t/1e9:.0f} GB/s")
+ref = (A.values, A.col_indices)
