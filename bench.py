@@ -157,10 +157,12 @@ def cpu_sample(A, b, iters):
 
 
 def cpu_calibrated(A, b, target_seconds):
-    it0, dt0 = cpu_sample(A, b, 3)
-    per = dt0 / max(it0, 1)
-    iters = int(max(5, min(400, target_seconds / max(per, 1e-6))))
-    return iters
+    """Window length K with ~target_seconds of CPU work.  The reorth cost of
+    iteration j grows linearly in j, so the window time grows ~K^2."""
+    k0 = 8
+    it0, dt0 = cpu_sample(A, b, k0)
+    iters = int(k0 * (max(target_seconds, 1e-3) / max(dt0, 1e-6)) ** 0.5)
+    return int(max(5, min(400, iters)))
 
 
 def run_reference(args):

@@ -35,6 +35,54 @@ int scratch(Ctx* c, size_t bytes, void** out) {
   return RCG_OK;
 }
 
+Pool::~Pool() { trim(); }
+
+void Pool::trim() {
+  std::lock_guard<std::mutex> g(mu);
+  for (auto& kv : free_) cudaFree(kv.second);
+  free_.clear();
+  free_bytes = 0;
+}
+
+void* Pool::get(size_t bytes) {
+  bytes = (bytes + 4095) & ~(size_t)4095;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = free_.lower_bound(bytes);
+    // best fit, but do not hand a huge idle block to a small request
+    if (it != free_.end() && it->first <= 2 * bytes + ((size_t)64 << 20)) {
+      void* p = it->second;
+      free_bytes -= it->first;
+      free_.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    trim();
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+  }
+  return p;
+}
+
+void Pool::put(void* p, size_t bytes) {
+  if (!p) return;
+  bytes = (bytes + 4095) & ~(size_t)4095;
+  std::lock_guard<std::mutex> g(mu);
+  free_.emplace(bytes, p);
+  free_bytes += bytes;
+  while (free_bytes > keep_bytes && !free_.empty()) {
+    auto it = std::prev(free_.end());
+    cudaFree(it->second);
+    free_bytes -= it->first;
+    free_.erase(it);
+  }
+}
+
 static cudaEvent_t pool_get(Ctx* c) {
   if (!c->event_pool.empty()) {
     cudaEvent_t e = c->event_pool.back();

@@ -22,6 +22,7 @@
 #include "dense.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <vector>
 
@@ -66,59 +67,118 @@ struct IterArgs {
 
 // Tile GEMV-T: partial dots of `ncols` columns (column k at base + k*ld, the
 // tile's first row already applied) with NV smem vectors of length len.
-// Warps own groups of CG consecutive columns, so each vector element loaded
-// from shared memory is reused for CG columns and each lane keeps CG*NV
-// independent accumulators (+ CG loads in flight per row step).
+// Work items are (group of CG consecutive columns) x (row slice); when there
+// are fewer column groups than warps the rows are split so every warp
+// streams.  Lanes read 2 consecutive rows with one 128-bit load per column
+// (base, ld and the tile start are 16-B aligned), so a lane keeps CG
+// LDG.128 in flight per step and reuses each smem vector element for CG
+// columns.  Slice partials are combined in smem in a fixed order.
 template <int CG, int NV>
 __device__ __forceinline__ void gemv_t_tile(const double* __restrict__ base, int64_t ld, int64_t ncols, int64_t len,
                                             const double* __restrict__ v0, const double* __restrict__ v1,
-                                            double* __restrict__ out) {
+                                            double* __restrict__ out, double* __restrict__ red /* smem kWarps*CG*NV */) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t ngroups = (ncols + CG - 1) / CG;
-  for (int64_t g = wid; g < ngroups; g += kWarps) {
-    const int64_t k0 = g * CG;
-    const int kc = (int)min((int64_t)CG, ncols - k0);
-    const double* __restrict__ cols = base + k0 * ld;
+  // row slices per group: enough items for every warp when groups are few
+  // (a power of two dividing kWarps, so the S slices of a group are always
+  // consecutive warps of the same round)
+  int S = 1;
+  while (S < kWarps && ngroups * S < kWarps) S *= 2;
+  const int64_t pairs = len >> 1;  // full row pairs
+  const int64_t per = (pairs + S - 1) / S;
+  const int64_t nitems = ngroups * S;
+  for (int64_t rnd = 0; rnd * kWarps < nitems; ++rnd) {
+    const int64_t item = rnd * kWarps + wid;
     double a0[CG], a1[CG];
 #pragma unroll
     for (int c = 0; c < CG; ++c) a0[c] = a1[c] = 0.0;
-    if (kc == CG) {
+    int64_t g = -1;
+    int sl = 0;
+    if (item < nitems) {
+      g = item / S;
+      sl = (int)(item % S);
+      const int64_t k0 = g * CG;
+      const int kc = (int)min((int64_t)CG, ncols - k0);
+      const double* __restrict__ cols = base + k0 * ld;
+      const int64_t p_begin = sl * per, p_end = min(pairs, p_begin + per);
+      if (kc == CG) {
 #pragma unroll 2
-      for (int64_t i = lane; i < len; i += 32) {
-        const double x0 = v0[i];
-        const double x1 = NV == 2 ? v1[i] : 0.0;
+        for (int64_t pi = p_begin + lane; pi < p_end; pi += 32) {
+          const double2 x0 = *reinterpret_cast<const double2*>(v0 + 2 * pi);
+          double2 x1 = make_double2(0.0, 0.0);
+          if (NV == 2) x1 = *reinterpret_cast<const double2*>(v1 + 2 * pi);
 #pragma unroll
-        for (int c = 0; c < CG; ++c) {
-          const double v = __ldcs(cols + c * ld + i);
-          a0[c] += v * x0;
-          if (NV == 2) a1[c] += v * x1;
+          for (int c = 0; c < CG; ++c) {
+            const double2 v = __ldcs(reinterpret_cast<const double2*>(cols + c * ld) + pi);
+            a0[c] += v.x * x0.x + v.y * x0.y;
+            if (NV == 2) a1[c] += v.x * x1.x + v.y * x1.y;
+          }
+        }
+      } else {
+        for (int64_t pi = p_begin + lane; pi < p_end; pi += 32) {
+          const double2 x0 = *reinterpret_cast<const double2*>(v0 + 2 * pi);
+          double2 x1 = make_double2(0.0, 0.0);
+          if (NV == 2) x1 = *reinterpret_cast<const double2*>(v1 + 2 * pi);
+#pragma unroll
+          for (int c = 0; c < CG; ++c)
+            if (c < kc) {
+              const double2 v = __ldcs(reinterpret_cast<const double2*>(cols + c * ld) + pi);
+              a0[c] += v.x * x0.x + v.y * x0.y;
+              if (NV == 2) a1[c] += v.x * x1.x + v.y * x1.y;
+            }
         }
       }
-    } else {
-      for (int64_t i = lane; i < len; i += 32) {
-        const double x0 = v0[i];
-        const double x1 = NV == 2 ? v1[i] : 0.0;
+      // odd tail row (len odd) belongs to the last slice
+      if ((len & 1) && sl == S - 1 && lane == 0) {
+        const int64_t i = len - 1;
 #pragma unroll
         for (int c = 0; c < CG; ++c)
           if (c < kc) {
-            const double v = __ldcs(cols + c * ld + i);
-            a0[c] += v * x0;
-            if (NV == 2) a1[c] += v * x1;
+            const double v = cols[c * ld + i];
+            a0[c] += v * v0[i];
+            if (NV == 2) a1[c] += v * v1[i];
           }
       }
-    }
 #pragma unroll
-    for (int c = 0; c < CG; ++c) {
-      a0[c] = warp_sum(a0[c]);
-      if (NV == 2) a1[c] = warp_sum(a1[c]);
+      for (int c = 0; c < CG; ++c) {
+        a0[c] = warp_sum(a0[c]);
+        if (NV == 2) a1[c] = warp_sum(a1[c]);
+      }
     }
-    if (lane == 0) {
+    if (S == 1) {
+      if (g >= 0 && lane == 0) {
+        const int64_t k0 = g * CG;
 #pragma unroll
-      for (int c = 0; c < CG; ++c)
-        if (c < kc) {
-          out[(k0 + c) * NV] = a0[c];
-          if (NV == 2) out[(k0 + c) * NV + 1] = a1[c];
+        for (int c = 0; c < CG; ++c)
+          if (k0 + c < ncols) {
+            out[(k0 + c) * NV] = a0[c];
+            if (NV == 2) out[(k0 + c) * NV + 1] = a1[c];
+          }
+      }
+    } else {
+      // combine the S slices of each group in slice order (deterministic)
+      if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < CG; ++c) {
+          red[(wid * CG + c) * NV] = a0[c];
+          if (NV == 2) red[(wid * CG + c) * NV + 1] = a1[c];
         }
+      }
+      __syncthreads();
+      if (g >= 0 && sl == 0 && lane == 0) {
+        const int64_t k0 = g * CG;
+        for (int c = 0; c < CG; ++c) {
+          if (k0 + c >= ncols) break;
+          double s0 = 0.0, s1 = 0.0;
+          for (int q = 0; q < S; ++q) {
+            s0 += red[((wid + q) * CG + c) * NV];
+            if (NV == 2) s1 += red[((wid + q) * CG + c) * NV + 1];
+          }
+          out[(k0 + c) * NV] = s0;
+          if (NV == 2) out[(k0 + c) * NV + 1] = s1;
+        }
+      }
+      __syncthreads();
     }
   }
 }
@@ -174,7 +234,9 @@ update_kernel(IterArgs a, int init) {
   if (threadIdx.x == 0) a.part_upd[(size_t)blockIdx.x * K] = rrb;
   if (a.n_c) {
     __syncthreads();
-    gemv_t_tile<4, 1>(a.AC + r0, a.ldac, a.n_c, r1 - r0, ytile, nullptr, a.part_upd + (size_t)blockIdx.x * K + 1);
+    __shared__ double red[kWarps * 8];
+    gemv_t_tile<8, 1>(a.AC + r0, a.ldac, a.n_c, r1 - r0, ytile, nullptr, a.part_upd + (size_t)blockIdx.x * K + 1,
+                      red);
   }
   if (arrive_last(a.counters + 1)) reduce_partials<kThreads>(a.part_upd, gridDim.x, (int)K, a.sums + 1);
 }
@@ -197,6 +259,7 @@ coarse_kernel(IterArgs a, int check_done) {
 // ---------------------------------------------------------------------------
 // K3: convergence test, z = M^{-1} r - C s, (r, z), reorth partials
 
+template <int CG>
 __global__ void __launch_bounds__(kThreads)
 precond_kernel(IterArgs a, int init) {
   SolveState* st = a.st;
@@ -263,8 +326,9 @@ precond_kernel(IterArgs a, int init) {
   if (reo) {
     __syncthreads();
     // AW is fully stored when reorthogonalizing (mod 0): column k at base + k*ld
-    gemv_t_tile<8, 2>(a.AW.base + r0, a.AW.ld, j + 1, r1 - r0, ztile, wtile,
-                      a.part_reo + (size_t)blockIdx.x * a.reo_stride);
+    __shared__ double red[kWarps * CG * 2];
+    gemv_t_tile<CG, 2>(a.AW.base + r0, a.AW.ld, j + 1, r1 - r0, ztile, wtile,
+                      a.part_reo + (size_t)blockIdx.x * a.reo_stride, red);
   }
   if (arrive_last(a.counters + 2)) reduce_partials<kThreads>(a.part_z, gridDim.x, 1, a.sums + a.rz_off);
 }
@@ -434,8 +498,15 @@ __global__ void copy_norms_kernel(int64_t n, const double* __restrict__ b, doubl
 // ---------------------------------------------------------------------------
 // host side
 
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 static int rows_per_block_for(const Ctx* c, int64_t n) {
-  int64_t rpt = ceil_div(n, (int64_t)kThreads * 2 * c->num_sms);
+  // ~4 row tiles per SM: the tile kernels run 3-4 CTAs/SM (45 KB smem, <= 64 regs)
+  static const int tiles_per_sm = env_int("RCG_TILES_PER_SM", 2);
+  int64_t rpt = ceil_div(n, (int64_t)kThreads * tiles_per_sm * c->num_sms);
   rpt = std::max<int64_t>(1, std::min<int64_t>(rpt, 16));
   return (int)(rpt * kThreads);
 }
@@ -473,7 +544,8 @@ using namespace rcg;
 
 struct rcg_trace {
   rcg_trace_view view{};
-  std::vector<void*> allocs;
+  std::vector<std::pair<void*, size_t>> allocs;   // returned to the pool on free
+  std::shared_ptr<rcg::Pool> pool;
   cudaStream_t stream = nullptr;
   int device = 0;
 };
@@ -490,8 +562,8 @@ extern "C" void rcg_trace_free(rcg_trace* t) {
   cudaGetDevice(&prev);
   cudaSetDevice(t->device);
   cudaStreamSynchronize(t->stream);
-  for (void* p : t->allocs)
-    if (p) cudaFree(p);
+  for (auto& pb : t->allocs)
+    if (pb.first) t->pool->put(pb.first, pb.second);
   cudaSetDevice(prev);
   delete t;
 }
@@ -499,36 +571,35 @@ extern "C" void rcg_trace_free(rcg_trace* t) {
 namespace {
 
 struct Grow {
-  // a column-major history buffer that grows geometrically
+  // a column-major history buffer that grows geometrically (pooled blocks)
   double* ptr = nullptr;
   int64_t cols = 0;
+  size_t bytes = 0;
 };
 
 int grow(Ctx* c, Grow& g, int64_t need_cols, int64_t ld, int64_t used_cols) {
   if (need_cols <= g.cols) return RCG_OK;
-  int64_t cols = std::max<int64_t>(need_cols, g.cols * 2);
-  double* p = nullptr;
-  cudaError_t e = cudaMalloc((void**)&p, sizeof(double) * (size_t)cols * ld);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    // retry at the exact requirement before giving up
+  int64_t cols = std::max<int64_t>(need_cols, g.cols + g.cols / 2);
+  size_t bytes = sizeof(double) * (size_t)cols * ld;
+  double* p = (double*)c->pool->get(bytes);
+  if (!p) {
     cols = need_cols;
-    e = cudaMalloc((void**)&p, sizeof(double) * (size_t)cols * ld);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
+    bytes = sizeof(double) * (size_t)cols * ld;
+    p = (double*)c->pool->get(bytes);
+    if (!p)
       return set_error(c, RCG_ERR_OOM, "out of device memory growing a Krylov history to %lld columns (%.2f GB)",
                        (long long)cols, 8.0 * cols * ld / 1e9);
-    }
   }
   if (g.ptr) {
     if (used_cols > 0)
       RCG_CUDA(c, cudaMemcpyAsync(p, g.ptr, sizeof(double) * (size_t)used_cols * ld, cudaMemcpyDeviceToDevice,
                                   c->stream));
     RCG_CUDA(c, cudaStreamSynchronize(c->stream));
-    cudaFree(g.ptr);
+    c->pool->put(g.ptr, g.bytes);
   }
   g.ptr = p;
   g.cols = cols;
+  g.bytes = bytes;
   return RCG_OK;
 }
 
@@ -553,17 +624,19 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
   rcg_trace* T = new rcg_trace();
   T->stream = c->stream;
   T->device = c->device;
+  T->pool = c->pool;
+  Grow gW, gAW, gZ, gR, gPR, gSum;
   auto fail = [&](int rc) {
+    for (Grow* g : {&gW, &gAW, &gZ, &gR, &gPR, &gSum})
+      if (g->ptr) c->pool->put(g->ptr, g->bytes);
     rcg_trace_free(T);
     return rc;
   };
   auto alloc = [&](size_t bytes, void** p) -> int {
-    cudaError_t e = cudaMalloc(p, std::max<size_t>(bytes, 256));
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return set_error(c, RCG_ERR_OOM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
-    }
-    T->allocs.push_back(*p);
+    bytes = std::max<size_t>(bytes, 256);
+    *p = c->pool->get(bytes);
+    if (!*p) return set_error(c, RCG_ERR_OOM, "device allocation of %zu bytes failed", bytes);
+    T->allocs.emplace_back(*p, bytes);
     return RCG_OK;
   };
 
@@ -596,9 +669,14 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
   double* wawd = hist + 4 * nh;
 
   // growable histories
-  Grow gW, gAW, gZ, gR, gPR, gSum;
   const bool storeW = reorth || store;
-  const int64_t init_cols = std::min<int64_t>(max_it + 2, 64);
+  // initial capacity from the previous solve of this size (sequences repeat)
+  int64_t hint = 64;
+  {
+    auto h = c->m_hint.find(n);
+    if (h != c->m_hint.end()) hint = std::max<int64_t>(64, h->second + h->second / 8 + 16);
+  }
+  const int64_t init_cols = std::min<int64_t>(max_it + 2, hint);
   if ((rc = grow(c, gW, storeW ? init_cols : 2, ld, 0))) return fail(rc);
   if ((rc = grow(c, gAW, reorth ? init_cols : 1, ld, 0))) return fail(rc);
   if ((rc = grow(c, gZ, capture ? init_cols : 2, ld, 0))) return fail(rc);
@@ -608,29 +686,29 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
   auto ensure_sums = [&](void) -> int {
     const int64_t need = 8 + n_c + 1 + 2 * reo_cols() + 8;
     if (gSum.cols < need) {
-      double* p = nullptr;
-      cudaError_t e = cudaMalloc((void**)&p, sizeof(double) * need);
-      if (e != cudaSuccess) return set_error(c, RCG_ERR_OOM, "sums alloc");
+      double* p = (double*)c->pool->get(sizeof(double) * need);
+      if (!p) return set_error(c, RCG_ERR_OOM, "sums alloc");
       RCG_CUDA(c, cudaMemsetAsync(p, 0, sizeof(double) * need, c->stream));
       if (gSum.ptr) {
         RCG_CUDA(c, cudaMemcpyAsync(p, gSum.ptr, sizeof(double) * gSum.cols, cudaMemcpyDeviceToDevice, c->stream));
         RCG_CUDA(c, cudaStreamSynchronize(c->stream));
-        cudaFree(gSum.ptr);
+        c->pool->put(gSum.ptr, gSum.bytes);
       }
       gSum.ptr = p;
       gSum.cols = need;
+      gSum.bytes = sizeof(double) * need;
     }
     if (reorth) {
       const int64_t needp = (int64_t)nb * 2 * reo_cols();
       if (gPR.cols < needp) {
         if (gPR.ptr) {
           RCG_CUDA(c, cudaStreamSynchronize(c->stream));
-          cudaFree(gPR.ptr);
+          c->pool->put(gPR.ptr, gPR.bytes);
         }
-        gPR.ptr = nullptr;
-        cudaError_t e = cudaMalloc((void**)&gPR.ptr, sizeof(double) * needp);
-        if (e != cudaSuccess) return set_error(c, RCG_ERR_OOM, "reorth partials alloc");
+        gPR.ptr = (double*)c->pool->get(sizeof(double) * needp);
+        if (!gPR.ptr) return set_error(c, RCG_ERR_OOM, "reorth partials alloc");
         gPR.cols = needp;
+        gPR.bytes = sizeof(double) * needp;
       }
     }
     return RCG_OK;
@@ -676,7 +754,9 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
   const size_t smem_pre = sizeof(double) * (2 * (size_t)R + n_c + 1);
   RCG_CUDA(c, cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(smem_upd, 1024)));
-  RCG_CUDA(c, cudaFuncSetAttribute(precond_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static const int pre_cg = env_int("RCG_PRE_CG", 8);
+  auto pre = pre_cg == 4 ? precond_kernel<4> : (pre_cg == 2 ? precond_kernel<2> : precond_kernel<8>);
+  RCG_CUDA(c, cudaFuncSetAttribute(pre, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(smem_pre, 1024)));
 
   // ---- initial guess and residual (solver.py:208-219) ----
@@ -719,12 +799,12 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
     T->view.AW = reorth ? gAW.ptr : nullptr;
     T->view.R = store ? gR.ptr : nullptr;
     T->view.waw = wawd;
-    T->allocs.push_back(gW.ptr);
-    T->allocs.push_back(gAW.ptr);
-    T->allocs.push_back(gZ.ptr);
-    T->allocs.push_back(gR.ptr);
-    T->allocs.push_back(gPR.ptr);
-    T->allocs.push_back(gSum.ptr);
+    T->allocs.emplace_back(gW.ptr, gW.bytes);
+    T->allocs.emplace_back(gAW.ptr, gAW.bytes);
+    T->allocs.emplace_back(gZ.ptr, gZ.bytes);
+    T->allocs.emplace_back(gR.ptr, gR.bytes);
+    T->allocs.emplace_back(gPR.ptr, gPR.bytes);
+    T->allocs.emplace_back(gSum.ptr, gSum.bytes);
     gW.ptr = gAW.ptr = gZ.ptr = gR.ptr = gPR.ptr = gSum.ptr = nullptr;
   };
 
@@ -752,7 +832,7 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
   update_kernel<<<nb, kThreads, smem_upd, c->stream>>>(a, 1);
   RCG_LAUNCH_CHECK(c);
   if ((rc = launch_coarse(1))) return fail(rc);
-  precond_kernel<<<nb, kThreads, smem_pre, c->stream>>>(a, 1);
+  pre<<<nb, kThreads, smem_pre, c->stream>>>(a, 1);
   RCG_LAUNCH_CHECK(c);
   init_finish_kernel<<<1, 1, 0, c->stream>>>(a);
   RCG_LAUNCH_CHECK(c);
@@ -812,7 +892,7 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
         prof_end(c);
       }
       prof_begin(c, RCG_K_PRECOND, 8.0 * nd * (2 + jac + n_c + (reorth ? 1.0 + js : 0.0)));
-      precond_kernel<<<nb, kThreads, smem_pre, c->stream>>>(a, 0);
+      pre<<<nb, kThreads, smem_pre, c->stream>>>(a, 0);
       RCG_LAUNCH_CHECK(c);
       prof_end(c);
       if (reorth) {
@@ -846,6 +926,7 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
   T->view.iterations = hst->converged ? hst->iterations : hst->j;
   if (hst->failure == RCG_FAIL_WAW) T->view.iterations = hst->j;
   T->view.n_betas = hst->converged ? T->view.iterations - 1 : hst->j;
+  c->m_hint[n] = T->view.iterations;
   finish_view();
   *trace_out = T;
   if (hst->failure) {

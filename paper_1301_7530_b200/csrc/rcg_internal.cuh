@@ -7,6 +7,9 @@
 #include <cstdio>
 #include <cstdarg>
 #include <vector>
+#include <map>
+#include <memory>
+#include <mutex>
 
 #include "../../include/rcg.h"
 
@@ -14,6 +17,23 @@ namespace rcg {
 
 constexpr int kThreads = 256;           // default CTA size for streaming kernels
 constexpr int kWarps = kThreads / 32;
+
+// ---------------------------------------------------------------------------
+// device buffer pool: Krylov histories are GBs per solve; recycling them
+// across the solves of a sequence avoids cudaMalloc/cudaFree of multi-GB
+// blocks (and the geometric-growth copies) on every system.  Shared by the
+// context and the traces it hands out (a trace may outlive its context).
+
+struct Pool {
+  std::mutex mu;
+  std::multimap<size_t, void*> free_;
+  size_t free_bytes = 0;
+  size_t keep_bytes = (size_t)96 << 30;  // cap on idle pooled memory
+  ~Pool();
+  void* get(size_t bytes);               // nullptr on OOM
+  void put(void* p, size_t bytes);
+  void trim();
+};
 
 // ---------------------------------------------------------------------------
 // context
@@ -41,6 +61,8 @@ struct Ctx {
   };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
+  std::shared_ptr<Pool> pool = std::make_shared<Pool>();
+  std::map<int64_t, int64_t> m_hint;     // n -> iterations of the last solve
 };
 
 // Brackets a launch with events when profiling; `collect` (after a stream

@@ -1,0 +1,38 @@
+"""Per-system wall/device time split of the config-2 sequence (diagnostic)."""
+import sys, time
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch
+import paper_1301_7530_b200 as rcg
+from paper_1301_7530_b200 import problems
+
+nelem = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+count = int(sys.argv[2]) if len(sys.argv) > 2 else 6
+seq = list(problems.elasticity_sequence(nelem, count, kind="fixed"))
+A = seq[0][0]
+bs = [torch.from_numpy(b).cuda() for _, b in seq]
+cfg = rcg.SolveConfig(tol=1e-8, max_iters=20000)
+strat = rcg.RecycleStrategy("srks", epsilon=1e-10, nc_limit=61)
+for rep_i in range(2):
+    torch.cuda.synchronize(); t0 = time.perf_counter()
+    state = rcg.AugmentationState.from_initial(A.n)
+    for k, b in enumerate(bs):
+        t1 = time.perf_counter()
+        D = rcg.guarded_deflation(A, state, [])
+        M = rcg.Preconditioner.jacobi(A)
+        torch.cuda.synchronize(); t2 = time.perf_counter()
+        x, tr = rcg.apcg_solve(A, M, D, b, cfg)
+        t3 = time.perf_counter()
+        spec = rcg.select_spectrum(tr, strat)
+        torch.cuda.synchronize(); t4 = time.perf_counter()
+        rcg.update_basis_srks(state, spec, k)
+        torch.cuda.synchronize(); t5 = time.perf_counter()
+        if state.n_c >= 61:
+            state.restart()
+        del tr, x
+        torch.cuda.synchronize(); t6 = time.perf_counter()
+        if rep_i == 1:
+            print(f"k={k} m={spec.m} nc={D.n_c} build={1e3*(t2-t1):.1f}ms solve_wall={1e3*(t3-t2):.1f}ms "
+                  f"select={1e3*(t4-t3):.1f}ms ritzvec={1e3*(t5-t4):.1f}ms free={1e3*(t6-t5):.1f}ms sel={int(spec.converged_mask.sum())}")
+    torch.cuda.synchronize()
+    print("total", time.perf_counter() - t0)

@@ -1,0 +1,6 @@
+#!/bin/bash
+# sweep kernel knobs on one config-2 solve; prints per-kernel GB/s
+for cg in 2 4 8; do for t in 2 4; do
+  echo -n "CG=$cg TILES=$t: "
+  RCG_PRE_CG=$cg RCG_TILES_PER_SM=$t timeout 200 python bench.py --systems 1 --steps 1 --warmup 1 --no-cpu --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); k=d['roofline']['all_kernels']; print(round(d['value'],1), {n:(round(v['seconds'],3), round(v['GBps'])) for n,v in k.items() if v['launches']})"
+done; done
