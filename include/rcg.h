@@ -48,15 +48,22 @@ typedef struct rcg_ctx rcg_ctx;
 typedef struct rcg_trace rcg_trace;
 
 /* CSR operator, full symmetric pattern (SparseSpdMatrix, core.py:34-111).
- * row_offsets is int32 when row_offsets_64 == 0, else int64; col_indices int32. */
+ * row_offsets is int32 when row_offsets_64 == 0, else int64; col_indices int32.
+ * block == 3: the optional bsr_* arrays hold the same operator as 3x3 blocks
+ * (built on device by rcg_csr_block3_build) and SpMV streams those instead:
+ * one column index per 9 values, ~29% fewer bytes for vector-valued FEM
+ * operators such as Q1 elasticity (BASELINE configs 2/3/5). */
 typedef struct {
   int64_t n;
   int64_t nnz;
   const void* row_offsets;
   int32_t row_offsets_64;
-  int32_t pad_;
+  int32_t block;                    /* 0 = scalar CSR only, 3 = bsr_* valid */
   const int32_t* col_indices;
   const double* values;
+  const int32_t* bsr_row_offsets;   /* [n/3 + 1] block-row offsets (blocks)   */
+  const int32_t* bsr_col_indices;   /* [nnz/9]   block column indices         */
+  const double* bsr_values;         /* [nnz]     9 per block, row-major       */
 } rcg_csr;
 
 /* Deflation operator P = I - C G^{-1} (AC)^T, G = C^T A C (DeflationOperator,
@@ -147,6 +154,12 @@ int rcg_spmm(rcg_ctx* ctx, const rcg_csr* A, const double* X, int64_t ldx,
  * Preconditioner.jacobi solver.py:39-41); either output may be NULL.
  * Returns RCG_ERR_CONTRACT if a diagonal entry is missing. */
 int rcg_csr_diagonal(rcg_ctx* ctx, const rcg_csr* A, double* diag, double* inv_diag);
+/* Does A (scalar CSR) have exact 3x3 block structure (n % 3 == 0, rows
+ * 3p..3p+2 share one column pattern made of aligned column triples)?
+ * Synchronizes; *is_block3_host = 0/1. */
+int rcg_csr_block3_analyze(rcg_ctx* ctx, const rcg_csr* A, int32_t* is_block3_host);
+/* Build the 3x3 BSR copy: bro[n/3+1], bci[nnz/9], bval[nnz]. */
+int rcg_csr_block3_build(rcg_ctx* ctx, const rcg_csr* A, int32_t* bro, int32_t* bci, double* bval);
 /* elementwise y = inv_diag * x (Preconditioner.apply, solver.py:50-54) */
 int rcg_diag_apply(rcg_ctx* ctx, int64_t n, const double* inv_diag, const double* x, double* y);
 

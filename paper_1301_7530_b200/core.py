@@ -75,11 +75,34 @@ def colmajor_from_host(M, ld=None):
 
 
 class _DevCsr:
-    __slots__ = ("ro", "ci", "va", "struct")
+    __slots__ = ("ro", "ci", "va", "bro", "bci", "bval", "struct")
 
     def __init__(self, ro, ci, va, n, nnz, ro64):
         self.ro, self.ci, self.va = ro, ci, va
-        self.struct = _lib.RcgCsr(n, nnz, ro.data_ptr(), 1 if ro64 else 0, 0, ci.data_ptr(), va.data_ptr())
+        self.bro = self.bci = self.bval = None
+        self.struct = _lib.RcgCsr(n, nnz, ro.data_ptr(), 1 if ro64 else 0, 0, ci.data_ptr(), va.data_ptr(),
+                                  None, None, None)
+
+    def add_block3(self, ctx):
+        """Detect 3x3 block structure on the device and attach a BSR copy
+        (SpMV then streams 8.4 instead of 12 bytes per nonzero)."""
+        torch = _torch()
+        flag = _lib.C.c_int32(0)
+        ctx.check(ctx.lib.rcg_csr_block3_analyze(ctx.h, _lib.C.byref(self.struct), _lib.C.byref(flag)),
+                  "block3_analyze")
+        if not flag.value:
+            return False
+        n, nnz = int(self.struct.n), int(self.struct.nnz)
+        self.bro = torch.empty(n // 3 + 1, dtype=torch.int32, device="cuda")
+        self.bci = torch.empty(max(nnz // 9, 1), dtype=torch.int32, device="cuda")
+        self.bval = torch.empty(max(nnz, 1), dtype=torch.float64, device="cuda")
+        ctx.check(ctx.lib.rcg_csr_block3_build(ctx.h, _lib.C.byref(self.struct), _lib.ptr(self.bro),
+                                               _lib.ptr(self.bci), _lib.ptr(self.bval)), "block3_build")
+        self.struct.bsr_row_offsets = self.bro.data_ptr()
+        self.struct.bsr_col_indices = self.bci.data_ptr()
+        self.struct.bsr_values = self.bval.data_ptr()
+        self.struct.block = 3
+        return True
 
 
 @dataclass(frozen=True, eq=False)
@@ -95,6 +118,7 @@ class SparseSpdMatrix:
     col_indices: np.ndarray
     values: np.ndarray
     validate: bool = field(default=True, repr=False, compare=False)
+    use_block3: bool = field(default=False, repr=False, compare=False)
 
     def __post_init__(self):
         ro = np.asarray(self.row_offsets, dtype=np.int64)
@@ -180,6 +204,8 @@ class SparseSpdMatrix:
             ci = torch.from_numpy(np.ascontiguousarray(self.col_indices, dtype=np.int32)).to("cuda")
             va = torch.from_numpy(self.values).to("cuda")
             h = _DevCsr(ro, ci, va, self.n, self.nnz, ro64)
+            if self.use_block3 and self.n % 3 == 0 and self.nnz % 9 == 0 and self.nnz >= 9 * self.n // 3 * 2:
+                h.add_block3(_lib.context())
             self._dev[dev] = h
         return h
 

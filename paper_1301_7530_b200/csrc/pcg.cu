@@ -847,8 +847,11 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
   int64_t batch = cfg->batch > 0 ? cfg->batch : 4;
   const int wu_grid = (int)std::max<int64_t>(1, ceil_div(n, (int64_t)kThreads * WU_RPT));
   const double jac = inv_diag ? 1.0 : 0.0;
-  const double bytes_spmv = 12.0 * (double)A->nnz + (A->row_offsets_64 ? 8.0 : 4.0) * (double)(n + 1) +
-                            16.0 * (double)n;
+  // algorithmic bytes of the format actually streamed (BSR3: one index per block)
+  const double bytes_spmv =
+      (A->block == 3 && A->bsr_row_offsets)
+          ? 8.0 * (double)A->nnz + 4.0 * (double)A->nnz / 9.0 + 4.0 * (double)(n / 3 + 1) + 16.0 * (double)n
+          : 12.0 * (double)A->nnz + (A->row_offsets_64 ? 8.0 : 4.0) * (double)(n + 1) + 16.0 * (double)n;
   bool done = false;
   while (it < max_it && !done) {
     const int64_t B = std::min<int64_t>(batch, max_it - it);

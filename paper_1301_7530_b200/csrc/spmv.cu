@@ -15,6 +15,7 @@
 #include "rcg_internal.cuh"
 #include "spmv.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace rcg {
@@ -32,18 +33,51 @@ spmv_kernel(int64_t n, const RO* __restrict__ ro, const int32_t* __restrict__ ci
   const double* __restrict__ x = xs.at(j);
   double* __restrict__ y = ys.at(j);
   constexpr int RPW = 32 / V;                 // rows per warp step
+  constexpr int U = V == 1 ? 8 : 12;          // fast path: <= U*V entries per row
   const int lane = threadIdx.x & 31;
   const int sub = lane % V;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   double acc0 = 0.0, acc1 = 0.0;
-  for (int64_t r0 = warp * RPW; r0 < n; r0 += nwarps * RPW) {
+  int64_t r0 = warp * RPW;
+  int64_t rs = 0, re = 0;
+  if (r0 < n) {
     const int64_t row = r0 + lane / V;
-    double s = 0.0;
     if (row < n) {
-      const int64_t rs = ro_at(ro, row), re = ro_at(ro, row + 1);
+      rs = ro_at(ro, row);
+      re = ro_at(ro, row + 1);
+    }
+  }
+  for (; r0 < n; r0 += nwarps * RPW) {
+    const int64_t row = r0 + lane / V;
+    // prefetch the next step's row range (hides one dependent latency)
+    int64_t nrs = 0, nre = 0;
+    {
+      const int64_t nrow = row + nwarps * RPW;
+      if (nrow < n) {
+        nrs = ro_at(ro, nrow);
+        nre = ro_at(ro, nrow + 1);
+      }
+    }
+    double s = 0.0;
+    const bool fast = __all_sync(0xffffffffu, (re - rs) <= (int64_t)U * V);
+    if (fast) {
+      // every index/value load of the row in flight at once, then every gather
+      int c[U];
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t k = rs + sub + (int64_t)u * V;
+        const bool ok = k < re;
+        c[u] = ok ? __ldg(ci + k) : 0;
+        v[u] = ok ? __ldcs(va + k) : 0.0;
+      }
+      double t[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int u = 0; u < U; ++u) t[u & 3] += v[u] * __ldg(x + c[u]);
+      s = (t[0] + t[1]) + (t[2] + t[3]);
+    } else if (row < n) {
       int64_t k = rs + sub;
-      // four independent accumulators for memory-level parallelism
       double s1 = 0.0, s2 = 0.0, s3 = 0.0;
       for (; k + 3 * V < re; k += 4 * V) {
         const int c0 = __ldg(ci + k), c1 = __ldg(ci + k + V), c2 = __ldg(ci + k + 2 * V), c3 = __ldg(ci + k + 3 * V);
@@ -71,6 +105,8 @@ spmv_kernel(int64_t n, const RO* __restrict__ ro, const int32_t* __restrict__ ci
       }
       y[row] = yv;
     }
+    rs = nrs;
+    re = nre;
   }
   if (MODE == 0) return;
   __shared__ double sm[kWarps];
@@ -83,6 +119,161 @@ spmv_kernel(int64_t n, const RO* __restrict__ ro, const int32_t* __restrict__ ci
     if (K == 2) part[(size_t)blockIdx.x * K + 1] = t1;
   }
   if (arrive_last(counter)) reduce_partials<kThreads>(part, gridDim.x, K, out);
+}
+
+// ---------------------------------------------------------------------------
+// 3x3 block (BSR) path for vector-valued FEM operators.  Warp per block row:
+// the row's 9*nb values are one contiguous, coalesced stream; lane v holds
+// value v -> block v/9, local row (v%9)/3, local col v%3; x is gathered 3
+// contiguous doubles per block column.  Three accumulators per lane (one per
+// local row) are reduced with shuffles; lanes 0..2 write y[3p..3p+2].
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads)
+bsr3_kernel(int64_t nbr, const int32_t* __restrict__ bro, const int32_t* __restrict__ bci,
+            const double* __restrict__ bv, ColSel xs, ColSel ys, const double* __restrict__ b,
+            const SolveState* st, double* part, unsigned int* counter, double* out) {
+  long long j = 0;
+  if (st) {
+    if (st->done) return;
+    j = st->j;
+  }
+  const double* __restrict__ x = xs.at(j);
+  double* __restrict__ y = ys.at(j);
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double d0 = 0.0, d1 = 0.0;
+  constexpr int UB = 8;  // fast path: <= 256 values (28 blocks) per block row
+  int64_t p = warp;
+  int64_t s = 0, e = 0;
+  if (p < nbr) {
+    s = __ldg(bro + p);
+    e = __ldg(bro + p + 1);
+  }
+  for (; p < nbr; p += nwarps) {
+    int64_t ns = 0, ne = 0;
+    if (p + nwarps < nbr) {
+      ns = __ldg(bro + p + nwarps);
+      ne = __ldg(bro + p + nwarps + 1);
+    }
+    const int64_t nv = 9 * (e - s);
+    const double* __restrict__ vals = bv + 9 * s;
+    const int32_t* __restrict__ cols = bci + s;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    if (nv <= 32 * UB) {
+      double v[UB];
+      int xi[UB];
+      int li[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int vv = lane + 32 * u;
+        const bool ok = vv < nv;
+        const int blk = vv / 9;
+        const int rem = vv - 9 * blk;
+        li[u] = rem / 3;
+        v[u] = ok ? __ldcs(vals + vv) : 0.0;
+        xi[u] = ok ? 3 * __ldg(cols + blk) + (rem - 3 * li[u]) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const double prod = v[u] * __ldg(x + xi[u]);
+        a0 += li[u] == 0 ? prod : 0.0;
+        a1 += li[u] == 1 ? prod : 0.0;
+        a2 += li[u] == 2 ? prod : 0.0;
+      }
+    } else {
+      for (int64_t vv = lane; vv < nv; vv += 32) {
+        const int64_t blk = vv / 9;
+        const int rem = (int)(vv - 9 * blk);
+        const int l = rem / 3;
+        const double prod = __ldcs(vals + vv) * __ldg(x + 3 * (int64_t)__ldg(cols + blk) + (rem - 3 * l));
+        a0 += l == 0 ? prod : 0.0;
+        a1 += l == 1 ? prod : 0.0;
+        a2 += l == 2 ? prod : 0.0;
+      }
+    }
+    a0 = warp_sum(a0);
+    a1 = warp_sum(a1);
+    a2 = warp_sum(a2);
+    if (lane < 3) {
+      const double s3 = lane == 0 ? a0 : (lane == 1 ? a1 : a2);
+      const int64_t row = 3 * p + lane;
+      double yv;
+      if (MODE == 2) {
+        const double bb = b[row];
+        yv = bb - s3;
+        d1 += bb * bb;
+        d0 += yv * yv;
+      } else {
+        yv = s3;
+        if (MODE == 1) d0 += x[row] * yv;
+      }
+      y[row] = yv;
+    }
+    s = ns;
+    e = ne;
+  }
+  if (MODE == 0) return;
+  __shared__ double sm[kWarps];
+  const double t0 = block_sum<kThreads>(d0, sm);
+  double t1 = 0.0;
+  if (MODE == 2) t1 = block_sum<kThreads>(d1, sm);
+  constexpr int K = MODE == 2 ? 2 : 1;
+  if (threadIdx.x == 0) {
+    part[(size_t)blockIdx.x * K] = t0;
+    if (K == 2) part[(size_t)blockIdx.x * K + 1] = t1;
+  }
+  if (arrive_last(counter)) reduce_partials<kThreads>(part, gridDim.x, K, out);
+}
+
+int bsr3_grid(Ctx* c, int64_t nbr) {
+  int64_t g = ceil_div(nbr, kWarps);
+  const int64_t cap = (int64_t)c->num_sms * 8;
+  return (int)std::max<int64_t>(1, std::min(g, cap));
+}
+
+// block-structure test, one thread per block row
+template <typename RO>
+__global__ void block3_check_kernel(int64_t nbr, const RO* __restrict__ ro, const int32_t* __restrict__ ci,
+                                    int* bad) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nbr; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s0 = ro[3 * p], s1 = ro[3 * p + 1], s2 = ro[3 * p + 2], s3 = ro[3 * p + 3];
+    const int64_t L = s1 - s0;
+    if (L % 3 != 0 || s2 - s1 != L || s3 - s2 != L) {
+      atomicExch(bad, 1);
+      continue;
+    }
+    for (int64_t t = 0; t < L; ++t) {
+      const int c0 = ci[s0 + t];
+      const bool lead = (t % 3) == 0;
+      if ((lead && (c0 % 3) != 0) || (!lead && c0 != ci[s0 + t - 1] + 1) || ci[s1 + t] != c0 || ci[s2 + t] != c0) {
+        atomicExch(bad, 1);
+        break;
+      }
+    }
+  }
+}
+
+template <typename RO>
+__global__ void block3_build_kernel(int64_t nbr, const RO* __restrict__ ro, const int32_t* __restrict__ ci,
+                                    const double* __restrict__ va, int32_t* bro, int32_t* bci, double* bval) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nbr; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s0 = ro[3 * p];
+    const int64_t L = ro[3 * p + 1] - s0;
+    const int64_t b0 = s0 / 9;  // 9 entries per block over the three rows
+    bro[p] = (int32_t)b0;
+    if (p == nbr - 1) bro[nbr] = (int32_t)((s0 + 3 * L) / 9);
+    for (int64_t t = 0; t < L / 3; ++t) {
+      bci[b0 + t] = ci[s0 + 3 * t] / 3;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int64_t src = ro[3 * p + i] + 3 * t;
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj) bval[9 * (b0 + t) + 3 * i + jj] = va[src + jj];
+      }
+    }
+  }
 }
 
 int spmv_width(const rcg_csr* A) {
@@ -136,6 +327,21 @@ static void launch_v(int V, int grid, cudaStream_t s, const rcg_csr* A, ColSel x
 
 int launch_spmv(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const double* b,
                 const SolveState* st, double* part, unsigned int* counter, double* out) {
+  if (A->block == 3 && A->bsr_row_offsets) {
+    const int64_t nbr = A->n / 3;
+    const int g = bsr3_grid(c, nbr);
+    if (mode == 0)
+      bsr3_kernel<0><<<g, kThreads, 0, c->stream>>>(nbr, A->bsr_row_offsets, A->bsr_col_indices, A->bsr_values, xs,
+                                                    ys, b, st, part, counter, out);
+    else if (mode == 1)
+      bsr3_kernel<1><<<g, kThreads, 0, c->stream>>>(nbr, A->bsr_row_offsets, A->bsr_col_indices, A->bsr_values, xs,
+                                                    ys, b, st, part, counter, out);
+    else
+      bsr3_kernel<2><<<g, kThreads, 0, c->stream>>>(nbr, A->bsr_row_offsets, A->bsr_col_indices, A->bsr_values, xs,
+                                                    ys, b, st, part, counter, out);
+    RCG_LAUNCH_CHECK(c);
+    return RCG_OK;
+  }
   const int V = spmv_width(A);
   const int grid = spmv_grid(c, A, V);
   if (A->row_offsets_64) {
@@ -151,7 +357,10 @@ int launch_spmv(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const 
   return RCG_OK;
 }
 
-int spmv_partials(Ctx* c, const rcg_csr* A) { return spmv_grid(c, A, spmv_width(A)); }
+int spmv_partials(Ctx* c, const rcg_csr* A) {
+  if (A->block == 3 && A->bsr_row_offsets) return bsr3_grid(c, A->n / 3);
+  return spmv_grid(c, A, spmv_width(A));
+}
 
 // ---------------------------------------------------------------------------
 // diagonal extraction (core.py:103-104) and Jacobi inverse (solver.py:39-41)
@@ -237,6 +446,45 @@ extern "C" int rcg_diag_apply(rcg_ctx* ctx, int64_t n, const double* inv_diag, c
   if (!ctx) return RCG_ERR_CONTRACT;
   if (n == 0) return RCG_OK;
   diag_apply_kernel<<<elementwise_grid(ctx, n), kThreads, 0, ctx->stream>>>(n, inv_diag, x, y);
+  RCG_LAUNCH_CHECK(ctx);
+  return RCG_OK;
+}
+
+extern "C" int rcg_csr_block3_analyze(rcg_ctx* ctx, const rcg_csr* A, int32_t* is_block3_host) {
+  if (!ctx || !A || !is_block3_host) return RCG_ERR_CONTRACT;
+  *is_block3_host = 0;
+  if (A->n == 0 || A->n % 3 != 0 || A->nnz % 9 != 0 || A->nnz / 9 >= (int64_t)1 << 31) return RCG_OK;
+  int* bad = nullptr;
+  int rc = scratch(ctx, 256, (void**)&bad);
+  if (rc) return rc;
+  RCG_CUDA(ctx, cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+  const int64_t nbr = A->n / 3;
+  const int g = elementwise_grid(ctx, nbr);
+  if (A->row_offsets_64)
+    block3_check_kernel<int64_t><<<g, kThreads, 0, ctx->stream>>>(nbr, (const int64_t*)A->row_offsets,
+                                                                  A->col_indices, bad);
+  else
+    block3_check_kernel<int32_t><<<g, kThreads, 0, ctx->stream>>>(nbr, (const int32_t*)A->row_offsets,
+                                                                  A->col_indices, bad);
+  RCG_LAUNCH_CHECK(ctx);
+  int h = 1;
+  RCG_CUDA(ctx, cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  RCG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  *is_block3_host = h ? 0 : 1;
+  return RCG_OK;
+}
+
+extern "C" int rcg_csr_block3_build(rcg_ctx* ctx, const rcg_csr* A, int32_t* bro, int32_t* bci, double* bval) {
+  if (!ctx || !A) return RCG_ERR_CONTRACT;
+  if (A->n % 3 != 0) return set_error(ctx, RCG_ERR_CONTRACT, "n must be a multiple of 3 for 3x3 blocks");
+  const int64_t nbr = A->n / 3;
+  const int g = elementwise_grid(ctx, nbr);
+  if (A->row_offsets_64)
+    block3_build_kernel<int64_t><<<g, kThreads, 0, ctx->stream>>>(nbr, (const int64_t*)A->row_offsets,
+                                                                  A->col_indices, A->values, bro, bci, bval);
+  else
+    block3_build_kernel<int32_t><<<g, kThreads, 0, ctx->stream>>>(nbr, (const int32_t*)A->row_offsets,
+                                                                  A->col_indices, A->values, bro, bci, bval);
   RCG_LAUNCH_CHECK(ctx);
   return RCG_OK;
 }

@@ -150,3 +150,22 @@ def test_gemm_tn_nn(rng):
     Out = torch.empty((7, n), dtype=torch.float64, device="cuda")
     ctx.check(ctx.lib.rcg_gemm_nn(ctx.h, n, a, 7, _lib.ptr(Xd), n, _lib.ptr(Qd), a, _lib.ptr(Out), n))
     np.testing.assert_allclose(Out.cpu().numpy().T, X @ Q, rtol=1e-12, atol=1e-11)
+
+
+def test_block3_spmv_matches_scalar_csr(rng):
+    """The device-built 3x3 BSR copy (SpMV format for Q1 elasticity) computes
+    the same product as the scalar CSR path and as scipy."""
+    E = np.exp(rng.standard_normal((5, 5, 5)))
+    A0 = problems.elasticity_q1(5, E=E)
+    A = rcg.SparseSpdMatrix(A0.n, A0.row_offsets, A0.col_indices, A0.values, validate=False, use_block3=True)
+    B = rcg.SparseSpdMatrix(A0.n, A0.row_offsets, A0.col_indices, A0.values, validate=False, use_block3=False)
+    assert A.device_csr().struct.block == 3
+    assert B.device_csr().struct.block == 0
+    x = rng.standard_normal(A.n)
+    ya, yb = rcg.spmv(A, x), rcg.spmv(B, x)
+    np.testing.assert_allclose(ya, yb, rtol=1e-13, atol=1e-13 * np.abs(yb).max())
+    _spmv_close(A, x)
+    # not block structured -> scalar path
+    L0 = problems.assemble_diffusion(np.ones((6, 6)))
+    L = rcg.SparseSpdMatrix(L0.n, L0.row_offsets, L0.col_indices, L0.values, validate=False, use_block3=True)
+    assert L.device_csr().struct.block == 0

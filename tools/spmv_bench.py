@@ -1,19 +1,20 @@
-"""Time rcg_spmv on a BASELINE matrix (CUDA events, L2 flushed by the matrix size).
-usage: RCG_SPMV_V=8 python tools/spmv_bench.py [elast64|diff256|lap128]"""
-import sys, time
+"""Time rcg_spmv on a BASELINE matrix (CUDA events; the matrix exceeds L2).
+usage: RCG_SPMV_V=8 python tools/spmv_bench.py [elast64|diff256|lap128] [csr|auto]"""
+import os, sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-import numpy as np
 import torch
-from paper_1301_7530_b200 import problems, _lib
+from paper_1301_7530_b200 import problems, _lib, SparseSpdMatrix
 
 which = sys.argv[1] if len(sys.argv) > 1 else "elast64"
+fmt = sys.argv[2] if len(sys.argv) > 2 else "auto"
 if which == "elast64":
     A = problems.elasticity_q1(64, validate=False)
 elif which == "diff256":
     A = next(problems.lognormal_diffusion_sequence(256, 1))[0]
 else:
     A = problems.shifted_laplacian_sequence(count=1)[0][0]
+A = SparseSpdMatrix(A.n, A.row_offsets, A.col_indices, A.values, validate=False, use_block3=(fmt == "bsr3"))
 h = A.device_csr()
 ctx = _lib.context()
 x = torch.randn(A.n, dtype=torch.float64, device="cuda")
@@ -29,7 +30,7 @@ for _ in range(N):
 e1.record()
 torch.cuda.synchronize()
 t = e0.elapsed_time(e1) / N * 1e-3
-byt = 12 * A.nnz + 4 * (A.n + 1) + 16 * A.n
-import os
-print(f"{which} V={os.environ.get('RCG_SPMV_V','auto')} n={A.n} nnz={A.nnz} t={t*1e6:.1f}us  {byt/t/1e9:.0f} GB/s")
-ref = (A.values, A.col_indices)
+blk = h.struct.block
+byt = (8 * A.nnz + 4 * A.nnz / 9 + 4 * (A.n // 3 + 1) + 16 * A.n) if blk == 3 else (12 * A.nnz + 4 * (A.n + 1) + 16 * A.n)
+print(f"{which} fmt={'bsr3' if blk == 3 else 'csr'} V={os.environ.get('RCG_SPMV_V','auto')} n={A.n} nnz={A.nnz} "
+      f"t={t*1e6:.1f}us {byt/t/1e9:.0f} GB/s (algorithmic {byt/1e6:.0f} MB)")
