@@ -62,7 +62,8 @@ struct IterArgs {
   unsigned int* counters;  // [0] spmv [1] update [2] precond [3..] misc
   SolveState* st;
   int reorth;
-  int rows_per_block;
+  int rows_per_block;      // K3 row tile
+  int rows_per_block_upd;  // K2 row tile (smaller: its AC^T y GEMV-T has few columns)
 };
 
 // Tile GEMV-T: partial dots of `ncols` columns (column k at base + k*ld, the
@@ -212,8 +213,8 @@ update_kernel(IterArgs a, int init) {
   }
   extern __shared__ double ytile[];
   __shared__ double sm[kWarps];
-  const int64_t r0 = (int64_t)blockIdx.x * a.rows_per_block;
-  const int64_t r1 = min(a.n, r0 + a.rows_per_block);
+  const int64_t r0 = (int64_t)blockIdx.x * a.rows_per_block_upd;
+  const int64_t r1 = min(a.n, r0 + a.rows_per_block_upd);
   const double* w = a.W.at(j);
   const double* aw = a.AW.at(j);
   double* rh = a.R.base ? a.R.at(j) : nullptr;
@@ -503,9 +504,15 @@ static int env_int(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
+static int rows_per_block_for(const Ctx* c, int64_t n, int tiles_per_sm);
+
 static int rows_per_block_for(const Ctx* c, int64_t n) {
-  // ~4 row tiles per SM: the tile kernels run 3-4 CTAs/SM (45 KB smem, <= 64 regs)
   static const int tiles_per_sm = env_int("RCG_TILES_PER_SM", 2);
+  return rows_per_block_for(c, n, tiles_per_sm);
+}
+
+static int rows_per_block_for(const Ctx* c, int64_t n, int tiles_per_sm) {
+  // ~4 row tiles per SM: the tile kernels run 3-4 CTAs/SM (45 KB smem, <= 64 regs)
   int64_t rpt = ceil_div(n, (int64_t)kThreads * tiles_per_sm * c->num_sms);
   rpt = std::max<int64_t>(1, std::min<int64_t>(rpt, 16));
   return (int)(rpt * kThreads);
@@ -642,6 +649,9 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
 
   const int R = rows_per_block_for(c, n);
   const int nb = (int)std::max<int64_t>(1, ceil_div(n, R));
+  static const int upd_tiles = env_int("RCG_UPD_TILES_PER_SM", 8);
+  const int Ru = rows_per_block_for(c, n, upd_tiles);
+  const int nbu = (int)std::max<int64_t>(1, ceil_div(n, Ru));
   const int nbs = spmv_partials(c, A);
 
   // fixed-size device allocations
@@ -655,7 +665,7 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
   if ((rc = alloc(sizeof(SolveState), (void**)&st))) return fail(rc);
   if ((rc = alloc(sizeof(double) * 5 * nh, (void**)&hist))) return fail(rc);
   if ((rc = alloc(sizeof(double) * ld, (void**)&r))) return fail(rc);
-  if ((rc = alloc(sizeof(double) * nb * (1 + n_c), (void**)&part_upd))) return fail(rc);
+  if ((rc = alloc(sizeof(double) * nbu * (1 + n_c), (void**)&part_upd))) return fail(rc);
   if ((rc = alloc(sizeof(double) * (nb + 2 * nbs + 64), (void**)&part_z))) return fail(rc);
   part_spmv = part_z + nb + 32;
   if ((rc = alloc(sizeof(double) * (n_c + 1), (void**)&s_ext))) return fail(rc);
@@ -747,10 +757,11 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
     a.st = st;
     a.reorth = reorth ? 1 : 0;
     a.rows_per_block = R;
+    a.rows_per_block_upd = Ru;
   };
   refresh();
 
-  const size_t smem_upd = sizeof(double) * (n_c ? R : 1);
+  const size_t smem_upd = sizeof(double) * (n_c ? Ru : 1);
   const size_t smem_pre = sizeof(double) * (2 * (size_t)R + n_c + 1);
   RCG_CUDA(c, cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(smem_upd, 1024)));
@@ -829,7 +840,7 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
   };
 
   // ---- z0, rz0, w0 (solver.py:221-231) ----
-  update_kernel<<<nb, kThreads, smem_upd, c->stream>>>(a, 1);
+  update_kernel<<<nbu, kThreads, smem_upd, c->stream>>>(a, 1);
   RCG_LAUNCH_CHECK(c);
   if ((rc = launch_coarse(1))) return fail(rc);
   pre<<<nb, kThreads, smem_pre, c->stream>>>(a, 1);
@@ -886,7 +897,7 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
       if ((rc = launch_spmv(c, A, 1, a.W, a.AW, nullptr, st, part_spmv, counters + 0, gSum.ptr))) return fail(rc);
       prof_end(c);
       prof_begin(c, RCG_K_UPDATE, 8.0 * nd * (6 + jac + n_c + (store ? 1 : 0)));
-      update_kernel<<<nb, kThreads, smem_upd, c->stream>>>(a, 0);
+      update_kernel<<<nbu, kThreads, smem_upd, c->stream>>>(a, 0);
       RCG_LAUNCH_CHECK(c);
       prof_end(c);
       if (n_c > NC_INLINE) {
