@@ -51,6 +51,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU sample duration")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of row sharding")
     return p.parse_args()
 
 
@@ -67,14 +68,15 @@ def workload(nelem, systems):
     return A, bs
 
 
-def config_dict(A, nelem, systems, world):
+def config_dict(A, nelem, systems, world, sharded=False):
     return {
         "workload": f"BASELINE config 2: Q1 elasticity {nelem}^3 elements, fixed A, {systems} traction RHS, "
                     "Jacobi APCG tol 1e-8, full reorth, SRKS eps=1e-10 nc_limit=61",
         "n": int(A.n), "nnz": int(A.nnz), "systems": systems, "strategy": "srks", "epsilon": 1e-10,
         "nc_limit": 61, "tol": 1e-8, "reorthogonalize": True, "preconditioner": "jacobi",
         "l2": "inputs larger than L2 (CSR 764 MB, Krylov histories GBs)",
-        "parallelism": "replicas" if world > 1 else "single",
+        "parallelism": (f"rows{world} (row-sharded, NCCL halo + allreduce)" if sharded else
+                        ("replicas" if world > 1 else "single")),
     }
 
 
@@ -228,6 +230,19 @@ def run_ours(args):
     A, bs = workload(args.nelem, args.systems)
     cfg = rcg.SolveConfig(tol=1e-8, max_iters=args.max_iters, reorthogonalize=True)
     strat = rcg.RecycleStrategy("srks", epsilon=1e-10, nc_limit=61)
+    A_global = A
+    sharded = world > 1 and not args.replicas
+    if sharded:
+        # row slabs (x-slabs of nodes), halo plan, NCCL communicator
+        from paper_1301_7530_b200 import distributed as D
+        bounds = D.partition_rows(A.row_offsets, world, align=3)
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        s0, s1 = A.row_offsets[r0], A.row_offsets[r1]
+        ro_l, lci, va, plan = D.build_local_system(A.row_offsets[r0:r1 + 1], A.col_indices[s0:s1],
+                                                   A.values[s0:s1], bounds, rank)
+        D.init_comm()
+        A = D.ShardedMatrix(ro_l, lci, va, plan, A_global.n)
+        bs = [b[r0:r1].copy() for b in bs]
     bs_dev = [torch.from_numpy(b).to("cuda") for b in bs]
     A.device_csr()
 
@@ -269,7 +284,8 @@ def run_ours(args):
         barrier()
     launches = _lib.total_launches() - l0
     sec = max_over_ranks(e0.elapsed_time(e1) * 1e-3)
-    value = world * iters / sec
+    # replicas: every rank solves the whole sequence (weak); sharded: one joint solve (strong)
+    value = (iters if sharded else world * iters) / sec
     per_system = rep.iterations()
     nc_hist = rep.n_c_history()
 
@@ -297,7 +313,7 @@ def run_ours(args):
 
     # e2e: public API with host arrays; CSR + RHS uploads and x downloads timed
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not sharded:
         ro, ci, va = A.row_offsets, A.col_indices, A.values
         h2d = 4 * (A.n + 1) + 4 * A.nnz + 8 * A.nnz + 8 * A.n * len(bs)
         e2e_iters, d2h = 0, 0
@@ -328,9 +344,9 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Q1 elasticity assembly + N(0,1) tractions)",
-            "config": config_dict(A, args.nelem, args.systems, world),
+            "config": config_dict(A_global, args.nelem, args.systems, world, sharded),
             "sequence_seconds": sec / args.steps, "iterations_per_system": per_system,
             "n_c_before": nc_hist, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk.summary(),

@@ -115,6 +115,24 @@ typedef struct {
   double device_seconds;        /* GPU time of the iteration loop            */
 } rcg_trace_view;
 
+/* Row-sharded execution (one process per GPU).  Rank `rank`
+ * owns n_local contiguous rows; the CSR it passes has local column indices
+ * 0..n_local-1 for owned columns and n_local.. for ghost columns, grouped by
+ * owner rank.  Every SpMV-input vector has room for n_ghost entries after its
+ * n_local owned entries (leading dimensions count them).  send_idx lists, per
+ * peer (send_off[q]..send_off[q+1]), the local entries that peer q reads;
+ * ghosts from peer q land at n_local + recv_off[q]. */
+typedef struct {
+  int32_t nranks;
+  int32_t rank;
+  int64_t n_local;
+  int64_t n_ghost;
+  const int32_t* send_idx;   /* device [send_off[nranks]] */
+  const int64_t* send_off;   /* HOST   [nranks + 1]       */
+  const int64_t* recv_off;   /* HOST   [nranks + 1]       */
+  double* send_buf;          /* device [send_off[nranks]] */
+} rcg_halo;
+
 /* ---- context ------------------------------------------------------------ */
 int rcg_ctx_create(int device, void* cuda_stream, rcg_ctx** out);
 void rcg_ctx_destroy(rcg_ctx* ctx);
@@ -143,6 +161,14 @@ typedef struct {
 int rcg_ctx_set_profiling(rcg_ctx* ctx, int enable);
 int rcg_ctx_kernel_stats(const rcg_ctx* ctx, rcg_kernel_stat* out_host, int n); /* n <= RCG_K_NUM */
 int rcg_ctx_reset_stats(rcg_ctx* ctx);
+
+/* NCCL communicator for sharded runs.  nccl_lib may be NULL (the copy
+ * already loaded in the process, else libnccl.so.2 from the loader path). */
+int rcg_comm_unique_id(const char* nccl_lib, void* id_out_host /* 128 bytes */);
+int rcg_comm_init(rcg_ctx* ctx, const char* nccl_lib, const void* id_host, int nranks, int rank);
+int rcg_comm_destroy(rcg_ctx* ctx);
+int rcg_allreduce_sum(rcg_ctx* ctx, double* buf, int64_t count);
+int rcg_halo_exchange(rcg_ctx* ctx, const rcg_halo* halo, double* vec);
 
 /* ---- operators (core.py) ------------------------------------------------- */
 /* y = A x  (spmv, core.py:114-119 / SparseSpdMatrix.__matmul__ core.py:110-111) */
@@ -194,6 +220,17 @@ int rcg_initial_guess(rcg_ctx* ctx, const rcg_deflation* D, const double* b, dou
 int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag,
                    const rcg_deflation* D, const double* b, double* x,
                    const rcg_solve_cfg* cfg, rcg_trace** trace_out);
+/* Sharded variant: A holds this rank's rows (local/ghost column numbering
+ * above), b/x/inv_diag are local slices, C/AC in D are local row blocks whose
+ * leading dimension has room for the ghosts.  Reductions are allreduced, so
+ * every rank sees the same alpha/beta/convergence and the same trace
+ * coefficients; histories are local row blocks. */
+int rcg_apcg_solve_sharded(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag,
+                           const rcg_deflation* D, const double* b, double* x,
+                           const rcg_solve_cfg* cfg, const rcg_halo* halo, rcg_trace** trace_out);
+int rcg_deflation_build_sharded(rcg_ctx* ctx, const rcg_csr* A, double* C, int64_t ldc,
+                                int64_t n_c, double* AC, int64_t ldac, double* L, double* Ginv,
+                                const rcg_halo* halo, int64_t* bad_col_host);
 int rcg_trace_get_view(const rcg_trace* trace, rcg_trace_view* out_host);
 void rcg_trace_free(rcg_trace* trace);
 

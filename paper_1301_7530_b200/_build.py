@@ -13,7 +13,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "librcg.so"
-SOURCES = ["api.cu", "spmv.cu", "dense.cu", "pcg.cu", "ritz.cu"]
+SOURCES = ["api.cu", "spmv.cu", "dense.cu", "pcg.cu", "ritz.cu", "comm.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -36,7 +36,7 @@ def build(force=False, verbose=True, extra=()):
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-Xptxas", "-v" if os.environ.get("RCG_PTXAS_VERBOSE") else "-O3",
            "-I", str(PKG.parent / "include"), "-o", str(LIB) + ".tmp",
-           *[str(CSRC / s) for s in SOURCES], *extra]
+           *[str(CSRC / s) for s in SOURCES], "-ldl", *extra]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

@@ -50,6 +50,12 @@ class RcgTraceView(C.Structure):
                 ("device_seconds", C.c_double)]
 
 
+class RcgHalo(C.Structure):
+    _fields_ = [("nranks", C.c_int32), ("rank", C.c_int32), ("n_local", C.c_int64), ("n_ghost", C.c_int64),
+                ("send_idx", C.c_void_p), ("send_off", C.c_void_p), ("recv_off", C.c_void_p),
+                ("send_buf", C.c_void_p)]
+
+
 class RcgKernelStat(C.Structure):
     _fields_ = [("launches", C.c_int64), ("seconds", C.c_double), ("bytes", C.c_double)]
 
@@ -72,6 +78,11 @@ SIGNATURES = {
     "rcg_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "rcg_ctx_kernel_stats": (C.c_int, [_vp, C.POINTER(RcgKernelStat), C.c_int]),
     "rcg_ctx_reset_stats": (C.c_int, [_vp]),
+    "rcg_comm_unique_id": (C.c_int, [C.c_char_p, _vp]),
+    "rcg_comm_init": (C.c_int, [_vp, C.c_char_p, _vp, C.c_int, C.c_int]),
+    "rcg_comm_destroy": (C.c_int, [_vp]),
+    "rcg_allreduce_sum": (C.c_int, [_vp, _vp, _i64]),
+    "rcg_halo_exchange": (C.c_int, [_vp, C.POINTER(RcgHalo), _vp]),
     "rcg_spmv": (C.c_int, [_vp, C.POINTER(RcgCsr), _vp, _vp]),
     "rcg_spmm": (C.c_int, [_vp, C.POINTER(RcgCsr), _vp, _i64, _i64, _vp, _i64]),
     "rcg_csr_diagonal": (C.c_int, [_vp, C.POINTER(RcgCsr), _vp, _vp]),
@@ -86,6 +97,10 @@ SIGNATURES = {
     "rcg_initial_guess": (C.c_int, [_vp, C.POINTER(RcgDeflation), _vp, _vp]),
     "rcg_apcg_solve": (C.c_int, [_vp, C.POINTER(RcgCsr), _vp, C.POINTER(RcgDeflation), _vp, _vp,
                                  C.POINTER(RcgSolveCfg), C.POINTER(_vp)]),
+    "rcg_apcg_solve_sharded": (C.c_int, [_vp, C.POINTER(RcgCsr), _vp, C.POINTER(RcgDeflation), _vp, _vp,
+                                         C.POINTER(RcgSolveCfg), C.POINTER(RcgHalo), C.POINTER(_vp)]),
+    "rcg_deflation_build_sharded": (C.c_int, [_vp, C.POINTER(RcgCsr), _vp, _i64, _i64, _vp, _i64, _vp, _vp,
+                                              C.POINTER(RcgHalo), c_int64_p]),
     "rcg_trace_get_view": (C.c_int, [_vp, C.POINTER(RcgTraceView)]),
     "rcg_trace_free": (None, [_vp]),
     "rcg_lanczos_tridiag": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _vp]),

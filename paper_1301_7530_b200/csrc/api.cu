@@ -1,5 +1,6 @@
 // Context management and error plumbing of the C ABI (include/rcg.h).
 #include "rcg_internal.cuh"
+#include "comm.cuh"
 
 #include <cstdlib>
 #include <cstring>
@@ -181,6 +182,7 @@ extern "C" int rcg_ctx_create(int device, void* stream, rcg_ctx** out) {
 extern "C" void rcg_ctx_destroy(rcg_ctx* c) {
   if (!c) return;
   cudaStreamSynchronize(c->stream);
+  comm_free(c);
   if (c->scratch) cudaFree(c->scratch);
   if (c->counters) cudaFree(c->counters);
   if (c->pinned) cudaFreeHost(c->pinned);

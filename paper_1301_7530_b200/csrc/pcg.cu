@@ -20,6 +20,7 @@
 #include "rcg_internal.cuh"
 #include "spmv.cuh"
 #include "dense.cuh"
+#include "comm.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -612,8 +613,9 @@ int grow(Ctx* c, Grow& g, int64_t need_cols, int64_t ld, int64_t used_cols) {
 
 }  // namespace
 
-extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, const rcg_deflation* D,
-                              const double* b, double* x, const rcg_solve_cfg* cfg, rcg_trace** trace_out) {
+static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, const rcg_deflation* D,
+                      const double* b, double* x, const rcg_solve_cfg* cfg, const rcg_halo* H,
+                      rcg_trace** trace_out) {
   if (!ctx || !A || !cfg || !trace_out) return RCG_ERR_CONTRACT;
   *trace_out = nullptr;
   Ctx* c = ctx;
@@ -622,7 +624,10 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
   if (!(cfg->tol > 0.0 && cfg->tol < 1.0)) return set_error(c, RCG_ERR_CONTRACT, "tol must be in (0, 1)");
   if (cfg->max_iters < 1) return set_error(c, RCG_ERR_CONTRACT, "max_iters must be >= 1");
   const int64_t n_c = D ? D->n_c : 0;
-  const int64_t ld = pad_ld(std::max<int64_t>(n, 1));
+  if (H && H->n_local != n) return set_error(ctx, RCG_ERR_CONTRACT, "halo n_local does not match the local rows");
+  const int64_t n_ghost = H ? H->n_ghost : 0;
+  // columns that feed the SpMV carry the ghost entries after the owned ones
+  const int64_t ld = pad_ld(std::max<int64_t>(n + n_ghost, 1));
   const bool reorth = cfg->reorthogonalize != 0;
   const bool store = cfg->store_directions != 0;
   const bool capture = cfg->trace_capture != 0;
@@ -779,16 +784,22 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
   double* norms2 = nullptr;  // ||r0||^2, ||b||^2
   if ((rc = alloc(sizeof(double) * 16, (void**)&norms2))) return fail(rc);
   if (n_c) {
-    // x0 = C G^{-1} C^T b; r0 = b - A x0
+    // x0 = C G^{-1} C^T b; r0 = b - A x0 (x0 needs its ghosts for the SpMV)
+    double* xext = nullptr;
+    if ((rc = alloc(sizeof(double) * ld, (void**)&xext))) return fail(rc);
     if ((rc = gemv_t(c, n, n_c, D->C, D->ldc, b, gSum.ptr + 2))) return fail(rc);
-    if ((rc = coarse_combine(c, D, gSum.ptr + 2, nullptr, x))) return fail(rc);
-    if ((rc = launch_spmv(c, A, 2, colsel(x), colsel(r), b, nullptr, part_spmv, counters + 0, norms2)))
+    if ((rc = allreduce_sum(c, gSum.ptr + 2, (size_t)n_c))) return fail(rc);
+    if ((rc = coarse_combine(c, D, gSum.ptr + 2, nullptr, xext))) return fail(rc);
+    if ((rc = halo_exchange(c, H, colsel(xext), nullptr, xext))) return fail(rc);
+    if ((rc = launch_spmv(c, A, 2, colsel(xext), colsel(r), b, nullptr, part_spmv, counters + 0, norms2)))
       return fail(rc);
+    RCG_CUDA(c, cudaMemcpyAsync(x, xext, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
   } else {
     copy_norms_kernel<<<elementwise_grid(c, n), kThreads, 0, c->stream>>>(n, b, r, x, part_spmv, counters + 0,
                                                                         norms2);
     RCG_LAUNCH_CHECK(c);
   }
+  if ((rc = allreduce_sum(c, norms2, 2))) return fail(rc);
   double hn[2] = {0.0, 0.0};
   RCG_CUDA(c, cudaMemcpyAsync(hn, norms2, sizeof(hn), cudaMemcpyDeviceToHost, c->stream));
   RCG_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -842,9 +853,11 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
   // ---- z0, rz0, w0 (solver.py:221-231) ----
   update_kernel<<<nbu, kThreads, smem_upd, c->stream>>>(a, 1);
   RCG_LAUNCH_CHECK(c);
+  if ((rc = allreduce_sum(c, gSum.ptr + 1, (size_t)(1 + n_c)))) return fail(rc);
   if ((rc = launch_coarse(1))) return fail(rc);
   pre<<<nb, kThreads, smem_pre, c->stream>>>(a, 1);
   RCG_LAUNCH_CHECK(c);
+  if ((rc = allreduce_sum(c, gSum.ptr + a.rz_off, 1))) return fail(rc);
   init_finish_kernel<<<1, 1, 0, c->stream>>>(a);
   RCG_LAUNCH_CHECK(c);
 
@@ -893,13 +906,19 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
       const int64_t jj = it + q;  // the device-side j unless the solve already stopped
       const double nd = (double)n, js = (double)(jj + 1);
       // algorithmic bytes per launch (each operand touched once)
+      if (H) {  // ghosts of w_j from the neighbouring slabs
+        double* wcol = gW.ptr + (storeW ? jj : jj % 2) * ld;
+        if ((rc = halo_exchange(c, H, a.W, st, wcol))) return fail(rc);
+      }
       prof_begin(c, RCG_K_SPMV, bytes_spmv);
       if ((rc = launch_spmv(c, A, 1, a.W, a.AW, nullptr, st, part_spmv, counters + 0, gSum.ptr))) return fail(rc);
       prof_end(c);
+      if ((rc = allreduce_sum(c, gSum.ptr, 1))) return fail(rc);
       prof_begin(c, RCG_K_UPDATE, 8.0 * nd * (6 + jac + n_c + (store ? 1 : 0)));
       update_kernel<<<nbu, kThreads, smem_upd, c->stream>>>(a, 0);
       RCG_LAUNCH_CHECK(c);
       prof_end(c);
+      if ((rc = allreduce_sum(c, gSum.ptr + 1, (size_t)(1 + n_c)))) return fail(rc);
       if (n_c > NC_INLINE) {
         prof_begin(c, RCG_K_COARSE, 8.0 * (double)n_c * (double)n_c);
         if ((rc = launch_coarse(1))) return fail(rc);
@@ -915,6 +934,8 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
         RCG_LAUNCH_CHECK(c);
         prof_end(c);
       }
+      // one packed allreduce: (r, z) and the 2(j+1) reorth dot products
+      if ((rc = allreduce_sum(c, gSum.ptr + a.rz_off, (size_t)(1 + (reorth ? 2 * (jj + 1) : 0))))) return fail(rc);
       prof_begin(c, RCG_K_WUPDATE, 8.0 * nd * (3 + (reorth ? js : 0.0)));
       wupdate_kernel<<<wu_grid, kThreads, 0, c->stream>>>(a);
       RCG_LAUNCH_CHECK(c);
@@ -951,20 +972,42 @@ extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_
   return RCG_OK;
 }
 
+extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, const rcg_deflation* D,
+                              const double* b, double* x, const rcg_solve_cfg* cfg, rcg_trace** trace_out) {
+  return solve_impl(ctx, A, inv_diag, D, b, x, cfg, nullptr, trace_out);
+}
+
+extern "C" int rcg_apcg_solve_sharded(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag,
+                                      const rcg_deflation* D, const double* b, double* x, const rcg_solve_cfg* cfg,
+                                      const rcg_halo* halo, rcg_trace** trace_out) {
+  if (!halo) return ctx ? set_error(ctx, RCG_ERR_CONTRACT, "sharded solve needs a halo plan") : RCG_ERR_CONTRACT;
+  return solve_impl(ctx, A, inv_diag, D, b, x, cfg, halo, trace_out);
+}
+
 // ---------------------------------------------------------------------------
 // deflation build / project / initial guess (solver.py:63-117)
 
-extern "C" int rcg_deflation_build(rcg_ctx* ctx, const rcg_csr* A, const double* C, int64_t ldc, int64_t n_c,
-                                   double* AC, int64_t ldac, double* L, double* Ginv, int64_t* bad_col_host) {
+static int deflation_build_impl(rcg_ctx* ctx, const rcg_csr* A, double* C, int64_t ldc, int64_t n_c, double* AC,
+                                int64_t ldac, double* L, double* Ginv, const rcg_halo* H, int64_t* bad_col_host) {
   if (!ctx || !A) return RCG_ERR_CONTRACT;
   if (bad_col_host) *bad_col_host = -1;
   if (n_c == 0) return RCG_OK;
   Ctx* c = ctx;
-  int rc = rcg_spmm(ctx, A, C, ldc, n_c, AC, ldac);          // AC = A C
+  int rc = RCG_OK;
+  if (H) {  // AC = A C column by column, each column's ghosts exchanged first
+    for (int64_t k = 0; k < n_c && !rc; ++k) {
+      double* col = C + k * ldc;
+      rc = halo_exchange(c, H, colsel(col), nullptr, col);
+      if (!rc) rc = rcg_spmv(ctx, A, col, AC + k * ldac);
+    }
+  } else {
+    rc = rcg_spmm(ctx, A, C, ldc, n_c, AC, ldac);           // AC = A C
+  }
   if (rc) return rc;
   double* G = nullptr;
   RCG_CUDA(c, cudaMallocAsync((void**)&G, sizeof(double) * (size_t)n_c * n_c, c->stream));
-  rc = gemm_tn(c, A->n, n_c, n_c, C, ldc, AC, ldac, G, 1);   // 0.5 (C^T AC + (C^T AC)^T)
+  rc = gemm_tn(c, A->n, n_c, n_c, C, ldc, AC, ldac, G, 1);   // 0.5 (C^T AC + (C^T AC)^T), local rows
+  if (!rc) rc = allreduce_sum(c, G, (size_t)(n_c * n_c));   // sum of the slabs' contributions
   if (!rc) {
     int64_t bad = -1;
     rc = cholesky(c, G, n_c, 1e-12, L, Ginv, &bad);        // pivot_rtol=1e-12 (solver.py:116)
@@ -973,6 +1016,17 @@ extern "C" int rcg_deflation_build(rcg_ctx* ctx, const rcg_csr* A, const double*
   cudaFreeAsync(G, c->stream);
   if (!rc) RCG_CUDA(c, cudaStreamSynchronize(c->stream));
   return rc;
+}
+
+extern "C" int rcg_deflation_build(rcg_ctx* ctx, const rcg_csr* A, const double* C, int64_t ldc, int64_t n_c,
+                                   double* AC, int64_t ldac, double* L, double* Ginv, int64_t* bad_col_host) {
+  return deflation_build_impl(ctx, A, (double*)C, ldc, n_c, AC, ldac, L, Ginv, nullptr, bad_col_host);
+}
+
+extern "C" int rcg_deflation_build_sharded(rcg_ctx* ctx, const rcg_csr* A, double* C, int64_t ldc, int64_t n_c,
+                                           double* AC, int64_t ldac, double* L, double* Ginv, const rcg_halo* halo,
+                                           int64_t* bad_col_host) {
+  return deflation_build_impl(ctx, A, C, ldc, n_c, AC, ldac, L, Ginv, halo, bad_col_host);
 }
 
 extern "C" int rcg_project(rcg_ctx* ctx, const rcg_deflation* D, const double* x, double* out) {

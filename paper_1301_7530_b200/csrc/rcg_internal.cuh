@@ -35,6 +35,8 @@ struct Pool {
   void trim();
 };
 
+struct Comm;  // comm.cu
+
 // ---------------------------------------------------------------------------
 // context
 
@@ -63,6 +65,7 @@ struct Ctx {
   std::vector<cudaEvent_t> event_pool;
   std::shared_ptr<Pool> pool = std::make_shared<Pool>();
   std::map<int64_t, int64_t> m_hint;     // n -> iterations of the last solve
+  Comm* comm = nullptr;                  // NCCL communicator (sharded runs)
 };
 
 // Brackets a launch with events when profiling; `collect` (after a stream

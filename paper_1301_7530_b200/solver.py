@@ -172,25 +172,27 @@ def _ptrv(t):
     return None if t is None else t.data_ptr()
 
 
-def _basis_to_device(C, n):
+def _basis_to_device(C, n, n_ext=None):
     """Accept a host (n, n_c) array, a device (n_c, ld) column-major block
-    (``DeviceBlock``) or a torch (n, n_c) tensor; return (Cd (n_c, ld), ld)."""
+    (``DeviceBlock``) or a torch (n, n_c) tensor; return (Cd (n_c, ld), ld).
+    ``n_ext`` (sharded runs) reserves room for the ghost entries."""
     torch = _torch()
+    n_ext = n if n_ext is None else n_ext
     if isinstance(C, DeviceBlock):
         return C.cols, C.ld
     if is_device_tensor(C):
         if C.ndim != 2 or C.shape[0] != n:
             raise ContractViolation("augmentation basis must be n x n_c with n_c <= n")
-        ld = pad_ld(n)
+        ld = pad_ld(n_ext)
         out = torch.zeros((C.shape[1], ld), dtype=torch.float64, device="cuda")
         out[:, :n] = C.t().to(torch.float64)
         return out, ld
     Ch = np.asarray(C, dtype=np.float64)
     if Ch.size == 0:
         Ch = Ch.reshape(n, 0)
-    if Ch.ndim != 2 or Ch.shape[0] != n or Ch.shape[1] > n:
+    if Ch.ndim != 2 or Ch.shape[0] != n or (Ch.shape[1] > n and n_ext == n):
         raise ContractViolation("augmentation basis must be n x n_c with n_c <= n")
-    ld = pad_ld(n)
+    ld = pad_ld(n_ext)
     return colmajor_from_host(Ch, ld), ld
 
 
@@ -209,12 +211,15 @@ def build_deflation(A: SparseSpdMatrix, C) -> DeflationOperator:
     """AC, sym(C^T A C) and its guarded Cholesky (pivot_rtol 1e-12) on device
     (``solver.py:100-117``).  Raises RankDeficient(column)."""
     torch = _torch()
+    sharded = hasattr(A, "plan")
     if isinstance(C, DeviceBlock):
-        if C.n != A.n or C.shape[1] > A.n:
+        if C.n != A.n or (C.shape[1] > A.n and not sharded):
             raise ContractViolation("augmentation basis must be n x n_c with n_c <= n")
+        if sharded and C.ld < A.n_ext:
+            raise ContractViolation("sharded basis needs room for the ghost entries (ld >= n_ext)")
         Cd, ld = C.cols, C.ld
     else:
-        Cd, ld = _basis_to_device(C, A.n)
+        Cd, ld = _basis_to_device(C, A.n, getattr(A, "n_ext", A.n))
     n_c = int(Cd.shape[0])
     if n_c == 0:
         return DeflationOperator(A.n, None, None, None, None, ld)
@@ -224,8 +229,13 @@ def build_deflation(A: SparseSpdMatrix, C) -> DeflationOperator:
     bad = _lib.C.c_int64(-1)
     ctx = _lib.context()
     h = A.device_csr()
-    rc = ctx.lib.rcg_deflation_build(ctx.h, _lib.C.byref(h.struct), _lib.ptr(Cd), ld, n_c, _lib.ptr(AC), ld,
-                                     _lib.ptr(L), _lib.ptr(Ginv), _lib.C.byref(bad))
+    if sharded:
+        rc = ctx.lib.rcg_deflation_build_sharded(ctx.h, _lib.C.byref(h.struct), _lib.ptr(Cd), ld, n_c, _lib.ptr(AC),
+                                                 ld, _lib.ptr(L), _lib.ptr(Ginv), _lib.C.byref(A.halo_struct()),
+                                                 _lib.C.byref(bad))
+    else:
+        rc = ctx.lib.rcg_deflation_build(ctx.h, _lib.C.byref(h.struct), _lib.ptr(Cd), ld, n_c, _lib.ptr(AC), ld,
+                                         _lib.ptr(L), _lib.ptr(Ginv), _lib.C.byref(bad))
     if rc == _lib.RCG_ERR_RANK_DEFICIENT:
         raise RankDeficient(int(bad.value))
     ctx.check(rc, "deflation_build")
@@ -446,8 +456,13 @@ def apcg_solve(A: SparseSpdMatrix, M: Preconditioner, D: DeflationOperator, b, c
                             int(bool(cfg.trace_capture)), int(bool(cfg.store_directions)), 0)
     th = _lib.C.c_void_p()
     t0 = time.perf_counter()
-    rc = ctx.lib.rcg_apcg_solve(ctx.h, _lib.C.byref(h.struct), _lib.ptr(inv), _lib.C.byref(D.struct),
-                                _lib.ptr(bv), _lib.ptr(x), _lib.C.byref(scfg), _lib.C.byref(th))
+    if hasattr(A, "plan"):
+        rc = ctx.lib.rcg_apcg_solve_sharded(ctx.h, _lib.C.byref(h.struct), _lib.ptr(inv), _lib.C.byref(D.struct),
+                                            _lib.ptr(bv), _lib.ptr(x), _lib.C.byref(scfg),
+                                            _lib.C.byref(A.halo_struct()), _lib.C.byref(th))
+    else:
+        rc = ctx.lib.rcg_apcg_solve(ctx.h, _lib.C.byref(h.struct), _lib.ptr(inv), _lib.C.byref(D.struct),
+                                    _lib.ptr(bv), _lib.ptr(x), _lib.C.byref(scfg), _lib.C.byref(th))
     if not th.value:
         ctx.check(rc, "apcg_solve")
         raise RuntimeError("apcg_solve returned no trace")

@@ -1,0 +1,94 @@
+"""Multi-process (gloo, world_size 2, CPU) tests of the row-sharded path's
+host logic: partition, halo plan, and the sharded communication schedule
+emulated in numpy, checked against the serial oracle."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_1301_7530_b200 import problems
+from paper_1301_7530_b200.distributed import partition_rows
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _problem(kind):
+    if kind == "elasticity":
+        A, b = next(problems.elasticity_sequence(5, 1, kind="fixed"))
+        return A, b, 3
+    kappa = np.exp(np.random.default_rng(7).standard_normal((12, 9, 7)))
+    A = problems.assemble_diffusion(kappa)
+    b = np.random.default_rng(8).standard_normal(A.n)
+    return A, b, 1
+
+
+def _worker(rank, world, port, kind, n_c, out_dir):
+    import torch.distributed as dist
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    from paper_1301_7530_b200.distributed import build_local_system, partition_rows
+    from sharded_emulation import Shard, sharded_apcg
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        A, b, align = _problem(kind)
+        bounds = partition_rows(A.row_offsets, world, align=align)
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        s, e = A.row_offsets[r0], A.row_offsets[r1]
+        ro = A.row_offsets[r0:r1 + 1]
+        ro_l, lci, va, plan = build_local_system(ro, A.col_indices[s:e], A.values[s:e], bounds, rank)
+        # plan symmetry: what I receive from q is what q sends me
+        counts = [None] * world
+        dist.all_gather_object(counts, (plan.send_off.tolist(), plan.recv_off.tolist()))
+        for q in range(world):
+            if q == rank:
+                continue
+            sent_by_q = counts[q][0][rank + 1] - counts[q][0][rank]
+            assert sent_by_q == plan.recv_off[q + 1] - plan.recv_off[q]
+        S = Shard(ro_l, lci, va, plan)
+        diag = A.to_dense().diagonal() if A.n < 3000 else None
+        inv = 1.0 / diag[r0:r1]
+        rng = np.random.default_rng(11)
+        Cg = rng.standard_normal((A.n, n_c))
+        x, m, alphas, conv = sharded_apcg(S, inv, Cg[r0:r1], b[r0:r1], 1e-9, 500)
+        np.save(os.path.join(out_dir, f"x{rank}.npy"), x)
+        np.save(os.path.join(out_dir, f"meta{rank}.npy"), np.array([m, int(conv), r0, r1] + list(alphas[:5])))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind,n_c", [("elasticity", 0), ("elasticity", 3), ("diffusion", 2)])
+def test_sharded_schedule_matches_serial_oracle(tmp_path, kind, n_c):
+    from oracle import recycg_oracle as orc
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), kind, n_c, str(tmp_path)), nprocs=world, join=True)
+    A, b, _ = _problem(kind)
+    Cg = np.random.default_rng(11).standard_normal((A.n, n_c))
+    inv = 1.0 / orc.diagonal(A)
+    xo, to = orc.apcg_solve(A, inv, orc.build_deflation(A, Cg), b, 1e-9, 500)
+    xs, metas = [], []
+    for r in range(world):
+        xs.append(np.load(tmp_path / f"x{r}.npy"))
+        metas.append(np.load(tmp_path / f"meta{r}.npy"))
+    x = np.concatenate(xs)
+    assert metas[0][0] == metas[1][0]                      # replicated stopping decision
+    assert abs(metas[0][0] - to.iterations) <= max(1, 0.02 * to.iterations)
+    np.testing.assert_allclose(metas[0][4:], to.alphas[:len(metas[0]) - 4], rtol=1e-10)
+    assert np.linalg.norm(x - xo) <= 1e-8 * np.linalg.norm(xo)
+
+
+def test_partition_rows_balanced_and_aligned():
+    A = problems.elasticity_q1(6)
+    for P in (2, 3, 4, 8):
+        bd = partition_rows(A.row_offsets, P, align=3)
+        assert bd[0] == 0 and bd[-1] == A.n and np.all(np.diff(bd) >= 0)
+        assert np.all(bd % 3 == 0)
+        nnz = np.diff(A.row_offsets[bd])
+        assert nnz.max() <= 1.2 * nnz.mean() + 81 * 3
