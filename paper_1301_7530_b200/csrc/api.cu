@@ -183,6 +183,9 @@ extern "C" void rcg_ctx_destroy(rcg_ctx* c) {
   if (!c) return;
   cudaStreamSynchronize(c->stream);
   comm_free(c);
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.second.first);
+  if (c->dargs) cudaFree(c->dargs);
+  if (c->capture_stream) cudaStreamDestroy(c->capture_stream);
   if (c->scratch) cudaFree(c->scratch);
   if (c->counters) cudaFree(c->counters);
   if (c->pinned) cudaFreeHost(c->pinned);

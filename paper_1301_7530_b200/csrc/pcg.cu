@@ -65,6 +65,8 @@ struct IterArgs {
   int reorth;
   int rows_per_block;      // K3 row tile
   int rows_per_block_upd;  // K2 row tile (smaller: its AC^T y GEMV-T has few columns)
+  int nb_pre;              // K3 grid (partials per column in part_reo)
+  SpmvArgs spmv;           // K1 arguments (device-resident, graph-replayable)
 };
 
 // Tile GEMV-T: partial dots of `ncols` columns (column k at base + k*ld, the
@@ -190,7 +192,8 @@ __device__ __forceinline__ void gemv_t_tile(const double* __restrict__ base, int
 // (initial residual: only ||r||^2 and AC^T y).
 
 __global__ void __launch_bounds__(kThreads)
-update_kernel(IterArgs a, int init) {
+update_kernel(const IterArgs* __restrict__ ap, int init) {
+  const IterArgs& a = *ap;
   SolveState* st = a.st;
   if (st->done) return;
   const long long j = st->j;
@@ -243,19 +246,22 @@ update_kernel(IterArgs a, int init) {
   if (arrive_last(a.counters + 1)) reduce_partials<kThreads>(a.part_upd, gridDim.x, (int)K, a.sums + 1);
 }
 
-// coarse solve s = G^{-1} (AC^T y) for n_c > NC_INLINE: one warp per row of Ginv
+// coarse solve s = G^{-1} (AC^T y) for n_c > NC_INLINE: one warp per row of
+// Ginv, grid-stride over rows (fixed grid: graph-replayable for any n_c)
 __global__ void __launch_bounds__(kThreads)
-coarse_kernel(IterArgs a, int check_done) {
+coarse_kernel(const IterArgs* __restrict__ ap, int check_done) {
+  const IterArgs& a = *ap;
   if (check_done && a.st->done) return;
   const int lane = threadIdx.x & 31;
-  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (row >= a.n_c) return;
-  const double* g = a.Ginv + row * a.n_c;   // symmetric: row == column
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const double* u = a.sums + 2;
-  double s = 0.0;
-  for (int64_t k = lane; k < a.n_c; k += 32) s += g[k] * u[k];
-  s = warp_sum(s);
-  if (lane == 0) a.s_ext[row] = s;
+  for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < a.n_c; row += nw) {
+    const double* g = a.Ginv + row * a.n_c;   // symmetric: row == column
+    double s = 0.0;
+    for (int64_t k = lane; k < a.n_c; k += 32) s += g[k] * u[k];
+    s = warp_sum(s);
+    if (lane == 0) a.s_ext[row] = s;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -263,7 +269,8 @@ coarse_kernel(IterArgs a, int check_done) {
 
 template <int CG>
 __global__ void __launch_bounds__(kThreads)
-precond_kernel(IterArgs a, int init) {
+precond_kernel(const IterArgs* __restrict__ ap, int init) {
+  const IterArgs& a = *ap;
   SolveState* st = a.st;
   if (st->done) return;
   const long long j = st->j;
@@ -335,25 +342,31 @@ precond_kernel(IterArgs a, int init) {
   if (arrive_last(a.counters + 2)) reduce_partials<kThreads>(a.part_z, gridDim.x, 1, a.sums + a.rz_off);
 }
 
-// K4: sums[rz_off+1+q] = sum_b part_reo[b][q], q < 2(j+1); 32 q per CTA x 8 b-groups
+// K4: sums[rz_off+1+q] = sum_b part_reo[b][q], q < 2(j+1); 32 q per CTA step x 8
+// b-groups; grid-stride over q with a fixed grid so the launch is graph-replayable
 __global__ void __launch_bounds__(256)
-colreduce_kernel(IterArgs a, int nb) {
+colreduce_kernel(const IterArgs* __restrict__ ap) {
+  const IterArgs& a = *ap;
   if (a.st->done) return;
   const long long j = a.st->j;
+  const int nb = a.nb_pre;
   const int64_t Q = 2 * (j + 1);
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int64_t q = (int64_t)blockIdx.x * 32 + tx;
   __shared__ double sm[8][33];
-  double s = 0.0;
-  if (q < Q)
-    for (int b = ty; b < nb; b += 8) s += __ldcg(a.part_reo + (size_t)b * a.reo_stride + q);
-  sm[ty][tx] = s;
-  __syncthreads();
-  if (ty == 0 && q < Q) {
-    double t = sm[0][tx];
+  for (int64_t q0 = (int64_t)blockIdx.x * 32; q0 < Q; q0 += (int64_t)gridDim.x * 32) {
+    const int64_t q = q0 + tx;
+    double s = 0.0;
+    if (q < Q)
+      for (int b = ty; b < nb; b += 8) s += __ldcg(a.part_reo + (size_t)b * a.reo_stride + q);
+    sm[ty][tx] = s;
+    __syncthreads();
+    if (ty == 0 && q < Q) {
+      double t = sm[0][tx];
 #pragma unroll
-    for (int g = 1; g < 8; ++g) t += sm[g][tx];
-    a.sums[a.rz_off + 1 + q] = t;
+      for (int g = 1; g < 8; ++g) t += sm[g][tx];
+      a.sums[a.rz_off + 1 + q] = t;
+    }
+    __syncthreads();
   }
 }
 
@@ -361,7 +374,8 @@ colreduce_kernel(IterArgs a, int nb) {
 // K5: beta, w_{j+1} = z + beta w_j  (- W c' with c' = (AW^T w)/diag)
 
 __global__ void __launch_bounds__(kThreads)
-wupdate_kernel(IterArgs a) {
+wupdate_kernel(const IterArgs* __restrict__ ap) {
+  const IterArgs& a = *ap;
   SolveState* st = a.st;
   if (st->done) return;
   const long long j = st->j;
@@ -428,7 +442,8 @@ wupdate_kernel(IterArgs a) {
 }
 
 // initial (r0, z0) guard: rz <= 0 -> NumericalFailure before the loop (solver.py:229-230)
-__global__ void init_finish_kernel(IterArgs a) {
+__global__ void init_finish_kernel(const IterArgs* __restrict__ ap) {
+  const IterArgs& a = *ap;
   SolveState* st = a.st;
   if (st->done) return;
   const double rz = a.sums[a.rz_off];
@@ -613,6 +628,12 @@ int grow(Ctx* c, Grow& g, int64_t need_cols, int64_t ld, int64_t used_cols) {
 
 }  // namespace
 
+// collectives only for sharded calls (a context may own a communicator and
+// still run unsharded solves)
+static inline int allreduce_h(const rcg_halo* H, Ctx* c, double* buf, size_t count) {
+  return H ? allreduce_sum(c, buf, count) : RCG_OK;
+}
+
 static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, const rcg_deflation* D,
                       const double* b, double* x, const rcg_solve_cfg* cfg, const rcg_halo* H,
                       rcg_trace** trace_out) {
@@ -730,6 +751,9 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   };
   if ((rc = ensure_sums())) return fail(rc);
 
+  if (!c->dargs && cudaMalloc(&c->dargs, 4096) != cudaSuccess) return fail(set_error(c, RCG_ERR_OOM, "args"));
+  static_assert(sizeof(IterArgs) <= 4096, "IterArgs too large");
+  IterArgs* dargs = (IterArgs*)c->dargs;
   IterArgs a{};
   auto refresh = [&]() {
     a.n = n;
@@ -763,11 +787,25 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     a.reorth = reorth ? 1 : 0;
     a.rows_per_block = R;
     a.rows_per_block_upd = Ru;
+    a.nb_pre = nb;
+    spmv_args_fill(A, &a.spmv);
+    a.spmv.xs = a.W;
+    a.spmv.ys = a.AW;
+    a.spmv.st = st;
+    a.spmv.part = part_spmv;
+    a.spmv.counter = counters + 0;
+    a.spmv.out = gSum.ptr;
+    // device copy read by every iteration kernel (pageable source: staged
+    // before return, so the host struct may change right after)
+    return cudaMemcpyAsync(dargs, &a, sizeof(IterArgs), cudaMemcpyHostToDevice, c->stream);
   };
-  refresh();
+  RCG_CUDA(c, refresh());
 
+  // dynamic smem sized by n_c bucket so graphs are reusable across the
+  // systems of a sequence (n_c changes from system to system)
+  const int64_t nc_bucket = ((n_c + 1 + 63) / 64) * 64;
   const size_t smem_upd = sizeof(double) * (n_c ? Ru : 1);
-  const size_t smem_pre = sizeof(double) * (2 * (size_t)R + n_c + 1);
+  const size_t smem_pre = sizeof(double) * (2 * (size_t)R + nc_bucket);
   RCG_CUDA(c, cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(smem_upd, 1024)));
   static const int pre_cg = env_int("RCG_PRE_CG", 8);
@@ -788,7 +826,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     double* xext = nullptr;
     if ((rc = alloc(sizeof(double) * ld, (void**)&xext))) return fail(rc);
     if ((rc = gemv_t(c, n, n_c, D->C, D->ldc, b, gSum.ptr + 2))) return fail(rc);
-    if ((rc = allreduce_sum(c, gSum.ptr + 2, (size_t)n_c))) return fail(rc);
+    if ((rc = allreduce_h(H, c, gSum.ptr + 2, (size_t)n_c))) return fail(rc);
     if ((rc = coarse_combine(c, D, gSum.ptr + 2, nullptr, xext))) return fail(rc);
     if ((rc = halo_exchange(c, H, colsel(xext), nullptr, xext))) return fail(rc);
     if ((rc = launch_spmv(c, A, 2, colsel(xext), colsel(r), b, nullptr, part_spmv, counters + 0, norms2)))
@@ -799,7 +837,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
                                                                         norms2);
     RCG_LAUNCH_CHECK(c);
   }
-  if ((rc = allreduce_sum(c, norms2, 2))) return fail(rc);
+  if ((rc = allreduce_h(H, c, norms2, 2))) return fail(rc);
   double hn[2] = {0.0, 0.0};
   RCG_CUDA(c, cudaMemcpyAsync(hn, norms2, sizeof(hn), cudaMemcpyDeviceToHost, c->stream));
   RCG_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -844,21 +882,21 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
 
   auto launch_coarse = [&](int check_done) -> int {
     if (n_c > NC_INLINE) {
-      coarse_kernel<<<(unsigned)ceil_div(n_c * 32, kThreads), kThreads, 0, c->stream>>>(a, check_done);
+      coarse_kernel<<<2 * c->num_sms, kThreads, 0, c->stream>>>(dargs, check_done);
       RCG_LAUNCH_CHECK(c);
     }
     return RCG_OK;
   };
 
   // ---- z0, rz0, w0 (solver.py:221-231) ----
-  update_kernel<<<nbu, kThreads, smem_upd, c->stream>>>(a, 1);
+  update_kernel<<<nbu, kThreads, smem_upd, c->stream>>>(dargs, 1);
   RCG_LAUNCH_CHECK(c);
-  if ((rc = allreduce_sum(c, gSum.ptr + 1, (size_t)(1 + n_c)))) return fail(rc);
+  if ((rc = allreduce_h(H, c, gSum.ptr + 1, (size_t)(1 + n_c)))) return fail(rc);
   if ((rc = launch_coarse(1))) return fail(rc);
-  pre<<<nb, kThreads, smem_pre, c->stream>>>(a, 1);
+  pre<<<nb, kThreads, smem_pre, c->stream>>>(dargs, 1);
   RCG_LAUNCH_CHECK(c);
-  if ((rc = allreduce_sum(c, gSum.ptr + a.rz_off, 1))) return fail(rc);
-  init_finish_kernel<<<1, 1, 0, c->stream>>>(a);
+  if ((rc = allreduce_h(H, c, gSum.ptr + a.rz_off, 1))) return fail(rc);
+  init_finish_kernel<<<1, 1, 0, c->stream>>>(dargs);
   RCG_LAUNCH_CHECK(c);
 
   // ---- the loop (solver.py:241-288), batched ----
@@ -876,6 +914,53 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
       (A->block == 3 && A->bsr_row_offsets)
           ? 8.0 * (double)A->nnz + 4.0 * (double)A->nnz / 9.0 + 4.0 * (double)(n / 3 + 1) + 16.0 * (double)n
           : 12.0 * (double)A->nnz + (A->row_offsets_64 ? 8.0 : 4.0) * (double)(n + 1) + 16.0 * (double)n;
+  static const int use_graphs = env_int("RCG_GRAPHS", 1);
+  const int cr_grid = 2 * c->num_sms;
+  // queue B iterations; `direct` allows the host-side per-iteration work
+  // (profiling events, halo exchanges with jj-dependent addresses)
+  auto launch_batch = [&](int64_t B, int64_t it0, bool direct) -> int {
+    int rc2;
+    for (int64_t q = 0; q < B; ++q) {
+      const int64_t jj = it0 + q;  // the device-side j unless the solve already stopped
+      const double nd = (double)n, js = (double)(jj + 1);
+      if (H && direct) {  // ghosts of w_j from the neighbouring slabs
+        double* wcol = gW.ptr + (storeW ? jj : jj % 2) * ld;
+        if ((rc2 = halo_exchange(c, H, a.W, st, wcol))) return rc2;
+      }
+      // algorithmic bytes per launch (each operand touched once; DESIGN.md §4)
+      if (direct) prof_begin(c, RCG_K_SPMV, bytes_spmv);
+      if ((rc2 = launch_spmv_ind(c, A, &dargs->spmv))) return rc2;
+      if (direct) prof_end(c);
+      if ((rc2 = allreduce_h(H, c, gSum.ptr, 1))) return rc2;
+      if (direct) prof_begin(c, RCG_K_UPDATE, 8.0 * nd * (6 + jac + n_c + (store ? 1 : 0)));
+      update_kernel<<<nbu, kThreads, smem_upd, c->stream>>>(dargs, 0);
+      RCG_LAUNCH_CHECK(c);
+      if (direct) prof_end(c);
+      if ((rc2 = allreduce_h(H, c, gSum.ptr + 1, (size_t)(1 + n_c)))) return rc2;
+      if (n_c > NC_INLINE) {
+        if (direct) prof_begin(c, RCG_K_COARSE, 8.0 * (double)n_c * (double)n_c);
+        if ((rc2 = launch_coarse(1))) return rc2;
+        if (direct) prof_end(c);
+      }
+      if (direct) prof_begin(c, RCG_K_PRECOND, 8.0 * nd * (2 + jac + n_c + (reorth ? 1.0 + js : 0.0)));
+      pre<<<nb, kThreads, smem_pre, c->stream>>>(dargs, 0);
+      RCG_LAUNCH_CHECK(c);
+      if (direct) prof_end(c);
+      if (reorth) {
+        if (direct) prof_begin(c, RCG_K_COLREDUCE, 8.0 * 2.0 * js * (nb + 1));
+        colreduce_kernel<<<cr_grid, 256, 0, c->stream>>>(dargs);
+        RCG_LAUNCH_CHECK(c);
+        if (direct) prof_end(c);
+      }
+      // one packed allreduce: (r, z) and the 2(j+1) reorth dot products
+      if ((rc2 = allreduce_h(H, c, gSum.ptr + a.rz_off, (size_t)(1 + (reorth ? 2 * (jj + 1) : 0))))) return rc2;
+      if (direct) prof_begin(c, RCG_K_WUPDATE, 8.0 * nd * (3 + (reorth ? js : 0.0)));
+      wupdate_kernel<<<wu_grid, kThreads, 0, c->stream>>>(dargs);
+      RCG_LAUNCH_CHECK(c);
+      if (direct) prof_end(c);
+    }
+    return RCG_OK;
+  };
   bool done = false;
   while (it < max_it && !done) {
     const int64_t B = std::min<int64_t>(batch, max_it - it);
@@ -900,46 +985,47 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     }
     if (regrown) {
       if ((rc = ensure_sums())) return fail(rc);
-      refresh();
+      RCG_CUDA(c, refresh());
     }
-    for (int64_t q = 0; q < B; ++q) {
-      const int64_t jj = it + q;  // the device-side j unless the solve already stopped
-      const double nd = (double)n, js = (double)(jj + 1);
-      // algorithmic bytes per launch (each operand touched once; DESIGN.md §4)
-      if (H) {  // ghosts of w_j from the neighbouring slabs
-        double* wcol = gW.ptr + (storeW ? jj : jj % 2) * ld;
-        if ((rc = halo_exchange(c, H, a.W, st, wcol))) return fail(rc);
+    const bool graph_ok = use_graphs && !c->profiling && !H;
+    if (graph_ok) {
+      // one graph per (shape, batch size): parameters are all device-resident
+      char key[256];
+      snprintf(key, sizeof(key), "%p|%lld|%d|%d|%d|%d|%zu|%zu|%d|%d|%lld|%d|%d", (void*)pre, (long long)n,
+               spmv_width(A), nbs, nb, nbu, smem_upd, smem_pre, reorth ? 1 : 0, n_c > NC_INLINE ? 1 : 0,
+               (long long)B, A->block, A->row_offsets_64);
+      cudaGraphExec_t exec = nullptr;
+      auto gi = c->graphs.find(key);
+      if (gi != c->graphs.end()) {
+        exec = gi->second.first;
+      } else {
+        cudaGraph_t graph = nullptr;
+        // capture on a private stream (the caller's may be the legacy default
+        // stream, which cannot capture); the graph is launched on c->stream
+        if (!c->capture_stream) RCG_CUDA(c, cudaStreamCreateWithFlags(&c->capture_stream, cudaStreamNonBlocking));
+        cudaStream_t user_stream = c->stream;
+        c->stream = c->capture_stream;
+        cudaError_t ce = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
+        if (ce != cudaSuccess) {
+          c->stream = user_stream;
+          return fail(set_error(c, RCG_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ce)));
+        }
+        const int64_t l0 = c->launches;
+        int crc = launch_batch(B, it, false);
+        ce = cudaStreamEndCapture(c->stream, &graph);
+        c->stream = user_stream;
+        if (crc) return fail(crc);
+        if (ce != cudaSuccess) return fail(set_error(c, RCG_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ce)));
+        ce = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ce != cudaSuccess) return fail(set_error(c, RCG_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ce)));
+        c->graphs[key] = std::make_pair(exec, c->launches - l0);
+        c->launches = l0;
       }
-      prof_begin(c, RCG_K_SPMV, bytes_spmv);
-      if ((rc = launch_spmv(c, A, 1, a.W, a.AW, nullptr, st, part_spmv, counters + 0, gSum.ptr))) return fail(rc);
-      prof_end(c);
-      if ((rc = allreduce_sum(c, gSum.ptr, 1))) return fail(rc);
-      prof_begin(c, RCG_K_UPDATE, 8.0 * nd * (6 + jac + n_c + (store ? 1 : 0)));
-      update_kernel<<<nbu, kThreads, smem_upd, c->stream>>>(a, 0);
-      RCG_LAUNCH_CHECK(c);
-      prof_end(c);
-      if ((rc = allreduce_sum(c, gSum.ptr + 1, (size_t)(1 + n_c)))) return fail(rc);
-      if (n_c > NC_INLINE) {
-        prof_begin(c, RCG_K_COARSE, 8.0 * (double)n_c * (double)n_c);
-        if ((rc = launch_coarse(1))) return fail(rc);
-        prof_end(c);
-      }
-      prof_begin(c, RCG_K_PRECOND, 8.0 * nd * (2 + jac + n_c + (reorth ? 1.0 + js : 0.0)));
-      pre<<<nb, kThreads, smem_pre, c->stream>>>(a, 0);
-      RCG_LAUNCH_CHECK(c);
-      prof_end(c);
-      if (reorth) {
-        prof_begin(c, RCG_K_COLREDUCE, 8.0 * 2.0 * js * (nb + 1));
-        colreduce_kernel<<<(unsigned)ceil_div(2 * (jj + 1), 32), 256, 0, c->stream>>>(a, nb);
-        RCG_LAUNCH_CHECK(c);
-        prof_end(c);
-      }
-      // one packed allreduce: (r, z) and the 2(j+1) reorth dot products
-      if ((rc = allreduce_sum(c, gSum.ptr + a.rz_off, (size_t)(1 + (reorth ? 2 * (jj + 1) : 0))))) return fail(rc);
-      prof_begin(c, RCG_K_WUPDATE, 8.0 * nd * (3 + (reorth ? js : 0.0)));
-      wupdate_kernel<<<wu_grid, kThreads, 0, c->stream>>>(a);
-      RCG_LAUNCH_CHECK(c);
-      prof_end(c);
+      RCG_CUDA(c, cudaGraphLaunch(exec, c->stream));
+      c->launches += c->graphs[key].second;
+    } else {
+      if ((rc = launch_batch(B, it, true))) return fail(rc);
     }
     it += B;
     RCG_CUDA(c, cudaMemcpyAsync(hst, st, sizeof(SolveState), cudaMemcpyDeviceToHost, c->stream));
@@ -1007,7 +1093,7 @@ static int deflation_build_impl(rcg_ctx* ctx, const rcg_csr* A, double* C, int64
   double* G = nullptr;
   RCG_CUDA(c, cudaMallocAsync((void**)&G, sizeof(double) * (size_t)n_c * n_c, c->stream));
   rc = gemm_tn(c, A->n, n_c, n_c, C, ldc, AC, ldac, G, 1);   // 0.5 (C^T AC + (C^T AC)^T), local rows
-  if (!rc) rc = allreduce_sum(c, G, (size_t)(n_c * n_c));   // sum of the slabs' contributions
+  if (!rc) rc = allreduce_h(H, c, G, (size_t)(n_c * n_c));   // sum of the slabs' contributions
   if (!rc) {
     int64_t bad = -1;
     rc = cholesky(c, G, n_c, 1e-12, L, Ginv, &bad);        // pivot_rtol=1e-12 (solver.py:116)

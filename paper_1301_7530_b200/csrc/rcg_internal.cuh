@@ -66,6 +66,9 @@ struct Ctx {
   std::shared_ptr<Pool> pool = std::make_shared<Pool>();
   std::map<int64_t, int64_t> m_hint;     // n -> iterations of the last solve
   Comm* comm = nullptr;                  // NCCL communicator (sharded runs)
+  void* dargs = nullptr;                 // device-resident solve arguments (graph replay)
+  cudaStream_t capture_stream = nullptr; // private stream for graph capture
+  std::map<std::string, std::pair<cudaGraphExec_t, int64_t>> graphs;  // key -> (exec, kernels)
 };
 
 // Brackets a launch with events when profiling; `collect` (after a stream

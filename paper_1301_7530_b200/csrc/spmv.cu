@@ -21,10 +21,10 @@
 namespace rcg {
 
 template <typename RO, int V, int MODE>
-__global__ void __launch_bounds__(kThreads)
-spmv_kernel(int64_t n, const RO* __restrict__ ro, const int32_t* __restrict__ ci,
-            const double* __restrict__ va, ColSel xs, ColSel ys, const double* __restrict__ b,
-            const SolveState* st, double* part, unsigned int* counter, double* out) {
+__device__ __forceinline__ void spmv_body(int64_t n, const RO* __restrict__ ro, const int32_t* __restrict__ ci,
+                                          const double* __restrict__ va, const ColSel& xs, const ColSel& ys,
+                                          const double* __restrict__ b, const SolveState* st, double* part,
+                                          unsigned int* counter, double* out) {
   long long j = 0;
   if (st) {
     if (st->done) return;
@@ -129,10 +129,10 @@ spmv_kernel(int64_t n, const RO* __restrict__ ro, const int32_t* __restrict__ ci
 // local row) are reduced with shuffles; lanes 0..2 write y[3p..3p+2].
 
 template <int MODE>
-__global__ void __launch_bounds__(kThreads)
-bsr3_kernel(int64_t nbr, const int32_t* __restrict__ bro, const int32_t* __restrict__ bci,
-            const double* __restrict__ bv, ColSel xs, ColSel ys, const double* __restrict__ b,
-            const SolveState* st, double* part, unsigned int* counter, double* out) {
+__device__ __forceinline__ void bsr3_body(int64_t nbr, const int32_t* __restrict__ bro,
+                                          const int32_t* __restrict__ bci, const double* __restrict__ bv,
+                                          const ColSel& xs, const ColSel& ys, const double* __restrict__ b,
+                                          const SolveState* st, double* part, unsigned int* counter, double* out) {
   long long j = 0;
   if (st) {
     if (st->done) return;
@@ -225,6 +225,36 @@ bsr3_kernel(int64_t nbr, const int32_t* __restrict__ bro, const int32_t* __restr
     if (K == 2) part[(size_t)blockIdx.x * K + 1] = t1;
   }
   if (arrive_last(counter)) reduce_partials<kThreads>(part, gridDim.x, K, out);
+}
+
+template <typename RO, int V, int MODE>
+__global__ void __launch_bounds__(kThreads)
+spmv_kernel(int64_t n, const RO* __restrict__ ro, const int32_t* __restrict__ ci,
+            const double* __restrict__ va, ColSel xs, ColSel ys, const double* __restrict__ b,
+            const SolveState* st, double* part, unsigned int* counter, double* out) {
+  spmv_body<RO, V, MODE>(n, ro, ci, va, xs, ys, b, st, part, counter, out);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads)
+bsr3_kernel(int64_t nbr, const int32_t* __restrict__ bro, const int32_t* __restrict__ bci,
+            const double* __restrict__ bv, ColSel xs, ColSel ys, const double* __restrict__ b,
+            const SolveState* st, double* part, unsigned int* counter, double* out) {
+  bsr3_body<MODE>(nbr, bro, bci, bv, xs, ys, b, st, part, counter, out);
+}
+
+// Indirect variants for the solve loop: every argument is read from a
+// device-resident SpmvArgs, so one captured CUDA graph serves every
+// iteration, batch and solve of a sequence (see pcg.cu).
+template <typename RO, int V>
+__global__ void __launch_bounds__(kThreads) spmv_kernel_ind(const SpmvArgs* __restrict__ sa) {
+  spmv_body<RO, V, 1>(sa->n, (const RO*)sa->ro, sa->ci, sa->va, sa->xs, sa->ys, nullptr, sa->st, sa->part,
+                      sa->counter, sa->out);
+}
+
+__global__ void __launch_bounds__(kThreads) bsr3_kernel_ind(const SpmvArgs* __restrict__ sa) {
+  bsr3_body<1>(sa->n / 3, sa->bro, sa->bci, sa->bval, sa->xs, sa->ys, nullptr, sa->st, sa->part, sa->counter,
+               sa->out);
 }
 
 int bsr3_grid(Ctx* c, int64_t nbr) {
@@ -355,6 +385,54 @@ int launch_spmv(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const 
   }
   RCG_LAUNCH_CHECK(c);
   return RCG_OK;
+}
+
+int launch_spmv_ind(Ctx* c, const rcg_csr* A, const SpmvArgs* dargs) {
+  if (A->block == 3 && A->bsr_row_offsets) {
+    bsr3_kernel_ind<<<bsr3_grid(c, A->n / 3), kThreads, 0, c->stream>>>(dargs);
+    RCG_LAUNCH_CHECK(c);
+    return RCG_OK;
+  }
+  const int V = spmv_width(A);
+  const int grid = spmv_grid(c, A, V);
+#define RCG_IND_CASE(RO, VV)                                                   \
+  case VV:                                                                     \
+    spmv_kernel_ind<RO, VV><<<grid, kThreads, 0, c->stream>>>(dargs);          \
+    break;
+  if (A->row_offsets_64) {
+    switch (V) {
+      RCG_IND_CASE(int64_t, 1)
+      RCG_IND_CASE(int64_t, 2)
+      RCG_IND_CASE(int64_t, 4)
+      RCG_IND_CASE(int64_t, 8)
+      RCG_IND_CASE(int64_t, 16)
+      default:
+        spmv_kernel_ind<int64_t, 32><<<grid, kThreads, 0, c->stream>>>(dargs);
+    }
+  } else {
+    switch (V) {
+      RCG_IND_CASE(int32_t, 1)
+      RCG_IND_CASE(int32_t, 2)
+      RCG_IND_CASE(int32_t, 4)
+      RCG_IND_CASE(int32_t, 8)
+      RCG_IND_CASE(int32_t, 16)
+      default:
+        spmv_kernel_ind<int32_t, 32><<<grid, kThreads, 0, c->stream>>>(dargs);
+    }
+  }
+#undef RCG_IND_CASE
+  RCG_LAUNCH_CHECK(c);
+  return RCG_OK;
+}
+
+void spmv_args_fill(const rcg_csr* A, SpmvArgs* s) {
+  s->n = A->n;
+  s->ro = A->row_offsets;
+  s->ci = A->col_indices;
+  s->va = A->values;
+  s->bro = A->bsr_row_offsets;
+  s->bci = A->bsr_col_indices;
+  s->bval = A->bsr_values;
 }
 
 int spmv_partials(Ctx* c, const rcg_csr* A) {

@@ -2,9 +2,27 @@
 #include "rcg_internal.cuh"
 
 namespace rcg {
+// device-resident SpMV arguments (mode 1: y = A x + (x, y)) for graph replay
+struct SpmvArgs {
+  int64_t n;
+  const void* ro;
+  const int32_t* ci;
+  const double* va;
+  const int32_t* bro;
+  const int32_t* bci;
+  const double* bval;
+  ColSel xs, ys;
+  const SolveState* st;
+  double* part;
+  unsigned int* counter;
+  double* out;
+};
+int launch_spmv_ind(Ctx* c, const rcg_csr* A, const SpmvArgs* dargs);
+void spmv_args_fill(const rcg_csr* A, SpmvArgs* s);
 // mode 0: y = A x; 1: y = A x + (x,y) -> out[0]; 2: y = b - A x + (y,y),(b,b) -> out[0..1]
 int launch_spmv(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const double* b,
                 const SolveState* st, double* part, unsigned int* counter, double* out);
-int spmv_partials(Ctx* c, const rcg_csr* A);  // number of partial slots per value
+int spmv_partials(Ctx* c, const rcg_csr* A);
+int spmv_width(const rcg_csr* A);  // number of partial slots per value
 int elementwise_grid(Ctx* c, int64_t n);
 }  // namespace rcg
