@@ -66,6 +66,7 @@ struct IterArgs {
   int rows_per_block;      // K3 row tile
   int rows_per_block_upd;  // K2 row tile (smaller: its AC^T y GEMV-T has few columns)
   int nb_pre;              // K3 grid (partials per column in part_reo)
+  double* part_wu;         // K5 column-split partial sums [S][n] (small n)
   SpmvArgs spmv;           // K1 arguments (device-resident, graph-replayable)
 };
 
@@ -276,9 +277,9 @@ precond_kernel(const IterArgs* __restrict__ ap, int init) {
   const long long j = st->j;
   if (!init) {
     const double rnorm = sqrt(a.sums[1]);
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.rnorms[j + 1] = rnorm;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) a.rnorms[j + 1] = rnorm;
     if (rnorm <= st->tol_abs) {                              // solver.py:273
-      if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
         st->converged = 1;
         st->iterations = j + 1;
         st->done = 1;
@@ -313,6 +314,10 @@ precond_kernel(const IterArgs* __restrict__ ap, int init) {
   double* w0 = init ? a.W.at(j) : nullptr;
   const double* wj = a.W.at(j);
   const bool reo = a.reorth && !init;
+  // column splits (small n): split 0 owns the z / (r, z) outputs, every split
+  // rebuilds the z tile and streams its share of the AW columns
+  const int split = blockIdx.y, S = gridDim.y;
+  const bool lead = split == 0;
   double rz = 0.0;
   for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
     const double ri = a.r[i];
@@ -322,8 +327,10 @@ precond_kernel(const IterArgs* __restrict__ ap, int init) {
       for (int64_t c = 0; c < a.n_c; ++c) cs += a.C[c * a.ldc + i] * s[c];
       zi = __dsub_rn(zi, cs);                               // y - C s  (solver.py:91)
     }
-    z[i] = zi;
-    if (w0) w0[i] = zi;                                     // w_0 = z_0 (solver.py:231)
+    if (lead) {
+      z[i] = zi;
+      if (w0) w0[i] = zi;                                   // w_0 = z_0 (solver.py:231)
+    }
     rz += ri * zi;
     if (reo) {
       ztile[i - r0] = zi;
@@ -331,15 +338,16 @@ precond_kernel(const IterArgs* __restrict__ ap, int init) {
     }
   }
   const double rzb = block_sum<kThreads>(rz, sm);
-  if (threadIdx.x == 0) a.part_z[blockIdx.x] = rzb;
+  if (lead && threadIdx.x == 0) a.part_z[blockIdx.x] = rzb;
   if (reo) {
     __syncthreads();
     // AW is fully stored when reorthogonalizing (mod 0): column k at base + k*ld
     __shared__ double red[kWarps * CG * 2];
-    gemv_t_tile<CG, 2>(a.AW.base + r0, a.AW.ld, j + 1, r1 - r0, ztile, wtile,
-                      a.part_reo + (size_t)blockIdx.x * a.reo_stride, red);
+    const long long kb = (j + 1) * split / S, ke = (j + 1) * (split + 1) / S;
+    gemv_t_tile<CG, 2>(a.AW.base + kb * a.AW.ld + r0, a.AW.ld, ke - kb, r1 - r0, ztile, wtile,
+                      a.part_reo + (size_t)blockIdx.x * a.reo_stride + 2 * kb, red);
   }
-  if (arrive_last(a.counters + 2)) reduce_partials<kThreads>(a.part_z, gridDim.x, 1, a.sums + a.rz_off);
+  if (lead && arrive_last(a.counters + 2)) reduce_partials<kThreads>(a.part_z, gridDim.x, 1, a.sums + a.rz_off);
 }
 
 // K4: sums[rz_off+1+q] = sum_b part_reo[b][q], q < 2(j+1); 32 q per CTA step x 8
@@ -382,32 +390,27 @@ wupdate_kernel(const IterArgs* __restrict__ ap) {
   const double rz_new = a.sums[a.rz_off];
   const double rz_old = st->rz;
   if (rz_new <= 0.0) {                                       // solver.py:279-280
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
       st->failure = RCG_FAIL_RZ;
       st->done = 1;
     }
     return;
   }
   const double beta = rz_new / rz_old;
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.betas[j] = beta;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) a.betas[j] = beta;
   __shared__ double cp[CP_CHUNK];
+  __shared__ bool s_last;
+  const int S = gridDim.y;           // column splits (small n: rows alone do not fill the GPU)
+  const int split = blockIdx.y;
   const int64_t r0 = (int64_t)blockIdx.x * (kThreads * WU_RPT);
-  const double* z = a.Z.at(j + 1);
-  const double* wo = a.W.at(j);
-  double* wn = a.W.at(j + 1);
-  double v[WU_RPT];
+  double acc[WU_RPT];
 #pragma unroll
-  for (int q = 0; q < WU_RPT; ++q) {
-    const int64_t i = r0 + threadIdx.x + q * kThreads;
-    v[q] = i < a.n ? __dadd_rn(z[i], __dmul_rn(beta, wo[i])) : 0.0;   // w = z + beta w
-  }
+  for (int q = 0; q < WU_RPT; ++q) acc[q] = 0.0;
   if (a.reorth) {
-    double acc[WU_RPT];
-#pragma unroll
-    for (int q = 0; q < WU_RPT; ++q) acc[q] = 0.0;
+    const long long kb = (j + 1) * split / S, ke = (j + 1) * (split + 1) / S;
     const double* red = a.sums + a.rz_off + 1;
-    for (long long k0 = 0; k0 <= j; k0 += CP_CHUNK) {
-      const long long kn = min((long long)CP_CHUNK, j + 1 - k0);
+    for (long long k0 = kb; k0 < ke; k0 += CP_CHUNK) {
+      const long long kn = min((long long)CP_CHUNK, ke - k0);
       __syncthreads();
       for (long long k = threadIdx.x; k < kn; k += kThreads) {
         const long long kk = k0 + k;
@@ -424,20 +427,67 @@ wupdate_kernel(const IterArgs* __restrict__ ap) {
           if (r0 + threadIdx.x + q * kThreads < a.n) acc[q] += col[q * kThreads] * ck;
       }
     }
-#pragma unroll
-    for (int q = 0; q < WU_RPT; ++q) v[q] = __dsub_rn(v[q], acc[q]);
   }
+  bool finisher = true;
+  if (S > 1) {
+    // park this split's partial sums; the last split of the row block adds
+    // them in split order (deterministic) and finishes the rows
 #pragma unroll
-  for (int q = 0; q < WU_RPT; ++q) {
-    const int64_t i = r0 + threadIdx.x + q * kThreads;
-    if (i < a.n) wn[i] = v[q];
-  }
-  if (arrive_last(a.counters + 4)) {
-    if (threadIdx.x == 0) {
-      st->rz = rz_new;
-      st->j = j + 1;
-      st->iterations = j + 1;
+    for (int q = 0; q < WU_RPT; ++q) {
+      const int64_t i = r0 + threadIdx.x + q * kThreads;
+      if (i < a.n) a.part_wu[(int64_t)split * a.n + i] = acc[q];
     }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned int* cnt = a.counters + 16 + blockIdx.x;
+      const unsigned int prev = atomicAdd(cnt, 1u);
+      s_last = (prev == (unsigned)S - 1);
+      if (s_last) *cnt = 0u;
+    }
+    __syncthreads();
+    finisher = s_last;
+    if (finisher) {
+      __threadfence();
+#pragma unroll
+      for (int q = 0; q < WU_RPT; ++q) {
+        const int64_t i = r0 + threadIdx.x + q * kThreads;
+        double t = 0.0;
+        if (i < a.n)
+          for (int sp = 0; sp < S; ++sp) t += __ldcg(a.part_wu + (int64_t)sp * a.n + i);
+        acc[q] = t;
+      }
+    }
+  }
+  if (finisher) {
+    const double* z = a.Z.at(j + 1);
+    const double* wo = a.W.at(j);
+    double* wn = a.W.at(j + 1);
+#pragma unroll
+    for (int q = 0; q < WU_RPT; ++q) {
+      const int64_t i = r0 + threadIdx.x + q * kThreads;
+      if (i < a.n) {
+        double v = __dadd_rn(z[i], __dmul_rn(beta, wo[i]));   // w = z + beta w
+        if (a.reorth) v = __dsub_rn(v, acc[q]);                // w -= W c'
+        wn[i] = v;
+      }
+    }
+  }
+  // the grid's last block advances the iteration (all blocks arrive once)
+  __shared__ bool g_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int prev = atomicAdd(a.counters + 4, 1u);
+    g_last = (prev == gridDim.x * gridDim.y - 1);
+    if (g_last) a.counters[4] = 0u;
+  }
+  __syncthreads();
+  if (g_last && threadIdx.x == 0) {
+    __threadfence();
+    st->rz = rz_new;
+    st->j = j + 1;
+    st->iterations = j + 1;
   }
 }
 
@@ -679,6 +729,11 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   const int Ru = rows_per_block_for(c, n, upd_tiles);
   const int nbu = (int)std::max<int64_t>(1, ceil_div(n, Ru));
   const int nbs = spmv_partials(c, A);
+  // K3 column splits for small n (the AW GEMV-T otherwise runs on nb CTAs only)
+  const int pre_split = reorth ? (int)std::max<int64_t>(1, std::min<int64_t>(8, (2 * c->num_sms) / nb)) : 1;
+  const int wu_grid = (int)std::max<int64_t>(1, ceil_div(n, (int64_t)kThreads * WU_RPT));
+  // K5 column splits when the row blocks alone cannot fill the SMs (small n)
+  const int wu_split = reorth ? (int)std::max<int64_t>(1, std::min<int64_t>(16, (2 * c->num_sms) / wu_grid)) : 1;
 
   // fixed-size device allocations
   SolveState* st = nullptr;
@@ -695,8 +750,11 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   if ((rc = alloc(sizeof(double) * (nb + 2 * nbs + 64), (void**)&part_z))) return fail(rc);
   part_spmv = part_z + nb + 32;
   if ((rc = alloc(sizeof(double) * (n_c + 1), (void**)&s_ext))) return fail(rc);
-  if ((rc = alloc(sizeof(unsigned int) * 16, (void**)&counters))) return fail(rc);
-  RCG_CUDA(c, cudaMemsetAsync(counters, 0, sizeof(unsigned int) * 16, c->stream));
+  const size_t n_counters = 16 + (size_t)wu_grid;
+  if ((rc = alloc(sizeof(unsigned int) * n_counters, (void**)&counters))) return fail(rc);
+  RCG_CUDA(c, cudaMemsetAsync(counters, 0, sizeof(unsigned int) * n_counters, c->stream));
+  double* part_wu = nullptr;
+  if (wu_split > 1 && (rc = alloc(sizeof(double) * (size_t)wu_split * n, (void**)&part_wu))) return fail(rc);
   RCG_CUDA(c, cudaMemsetAsync(hist, 0, sizeof(double) * 5 * nh, c->stream));
   double* alphas = hist;
   double* betas = hist + nh;
@@ -781,6 +839,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     a.part_upd = part_upd;
     a.part_z = part_z;
     a.part_reo = gPR.ptr;
+    a.part_wu = part_wu;
     a.reo_stride = 2 * reo_cols();
     a.counters = counters;
     a.st = st;
@@ -907,7 +966,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   SolveState* hst = (SolveState*)c->pinned;
   int64_t it = 0;
   int64_t batch = cfg->batch > 0 ? cfg->batch : 4;
-  const int wu_grid = (int)std::max<int64_t>(1, ceil_div(n, (int64_t)kThreads * WU_RPT));
+
   const double jac = inv_diag ? 1.0 : 0.0;
   // algorithmic bytes of the format actually streamed (BSR3: one index per block)
   const double bytes_spmv =
@@ -943,7 +1002,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
         if (direct) prof_end(c);
       }
       if (direct) prof_begin(c, RCG_K_PRECOND, 8.0 * nd * (2 + jac + n_c + (reorth ? 1.0 + js : 0.0)));
-      pre<<<nb, kThreads, smem_pre, c->stream>>>(dargs, 0);
+      pre<<<dim3(nb, pre_split), kThreads, smem_pre, c->stream>>>(dargs, 0);
       RCG_LAUNCH_CHECK(c);
       if (direct) prof_end(c);
       if (reorth) {
@@ -955,7 +1014,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
       // one packed allreduce: (r, z) and the 2(j+1) reorth dot products
       if ((rc2 = allreduce_h(H, c, gSum.ptr + a.rz_off, (size_t)(1 + (reorth ? 2 * (jj + 1) : 0))))) return rc2;
       if (direct) prof_begin(c, RCG_K_WUPDATE, 8.0 * nd * (3 + (reorth ? js : 0.0)));
-      wupdate_kernel<<<wu_grid, kThreads, 0, c->stream>>>(dargs);
+      wupdate_kernel<<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
       RCG_LAUNCH_CHECK(c);
       if (direct) prof_end(c);
     }
