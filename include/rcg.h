@@ -81,7 +81,10 @@ typedef struct {
 } rcg_deflation;
 
 /* SolveConfig (solver.py:125-139) plus the launch batch (iterations queued
- * between two host polls of the device-side convergence flag; 0 = auto). */
+ * between two host polls of the device-side convergence flag; 0 = auto) and
+ * krylov_cap (extension, 0 = none): keep only z_0..z_{cap-1} — Ritz
+ * extraction then runs on the leading cap x cap Lanczos block (SURVEY.md
+ * §8(c) "capped variants"; config 5 "stored Krylov basis up to 400 vecs"). */
 typedef struct {
   double tol;
   int64_t max_iters;
@@ -89,6 +92,7 @@ typedef struct {
   int32_t trace_capture;
   int32_t store_directions;
   int32_t batch;
+  int64_t krylov_cap;
 } rcg_solve_cfg;
 
 /* Read-only view of a finished solve (SolveTrace, solver.py:142-162). */
@@ -106,7 +110,7 @@ typedef struct {
   const double* betas;          /* [m]   device */
   const double* rz_inner;       /* [m]   device */
   const double* residual_norms; /* [m+1] device */
-  const double* Z;              /* z_0..z_{m-1} (trace_capture), ld = ld      */
+  const double* Z;              /* z_0..z_{min(m,cap)-1} (trace_capture), ld  */
   const double* W;              /* w_0..w_{m-1} (reorth or store_directions)  */
   const double* AW;             /* A w_j        (reorth)                      */
   const double* R;              /* r_0..r_{m-1} (store_directions)            */

@@ -14,7 +14,9 @@ import numpy as np
 
 from .core_errors import ContractViolation, NumericalFailure, RankDeficient
 
-_LIB_PATH = Path(__file__).resolve().parent / "librcg.so"
+import os as _os
+# RCG_LIB overrides the library path (A/B comparisons of builds on one box)
+_LIB_PATH = Path(_os.environ.get("RCG_LIB") or (Path(__file__).resolve().parent / "librcg.so"))
 
 RCG_OK, RCG_ERR_CONTRACT, RCG_ERR_RANK_DEFICIENT, RCG_ERR_NUMERICAL, RCG_ERR_CUDA, RCG_ERR_OOM = range(6)
 FAIL_NONE, FAIL_RZ, FAIL_WAW = 0, 1, 2
@@ -37,7 +39,8 @@ class RcgDeflation(C.Structure):
 
 class RcgSolveCfg(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_iters", C.c_int64), ("reorthogonalize", C.c_int32),
-                ("trace_capture", C.c_int32), ("store_directions", C.c_int32), ("batch", C.c_int32)]
+                ("trace_capture", C.c_int32), ("store_directions", C.c_int32), ("batch", C.c_int32),
+                ("krylov_cap", C.c_int64)]
 
 
 class RcgTraceView(C.Structure):

@@ -1,6 +1,7 @@
 // Context management and error plumbing of the C ABI (include/rcg.h).
 #include "rcg_internal.cuh"
 #include "comm.cuh"
+#include "vmm.cuh"
 
 #include <cstdlib>
 #include <cstring>
@@ -175,6 +176,9 @@ extern "C" int rcg_ctx_create(int device, void* stream, rcg_ctx** out) {
     delete c;
     return RCG_ERR_CUDA;
   }
+  c->chunks = std::make_shared<ChunkPool>();
+  c->chunks->device = device;
+  c->vpool = std::make_shared<VmmPool>();
   *out = c;
   return RCG_OK;
 }

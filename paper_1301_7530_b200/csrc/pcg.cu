@@ -21,6 +21,7 @@
 #include "spmv.cuh"
 #include "dense.cuh"
 #include "comm.cuh"
+#include "vmm.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -65,7 +66,9 @@ struct IterArgs {
   int reorth;
   int rows_per_block;      // K3 row tile
   int rows_per_block_upd;  // K2 row tile (smaller: its AC^T y GEMV-T has few columns)
-  int nb_pre;              // K3 grid (partials per column in part_reo)
+  int nb_pre;              // K3 row tiles (partial rows in part_reo / part_z)
+  int nb_upd;              // K2 row tiles
+  int nb_wu;               // K5 row blocks
   double* part_wu;         // K5 column-split partial sums [S][n] (small n)
   SpmvArgs spmv;           // K1 arguments (device-resident, graph-replayable)
 };
@@ -290,9 +293,10 @@ precond_kernel(const IterArgs* __restrict__ ap, int init) {
   extern __shared__ double dyn[];
   __shared__ double sm[kWarps];
   const int R = a.rows_per_block;
-  double* ztile = dyn;            // R
-  double* wtile = dyn + R;        // R
-  double* s = dyn + 2 * R;        // n_c
+  const int RT = a.reorth ? R : 0;
+  double* ztile = dyn;            // R (reorth only)
+  double* wtile = dyn + RT;       // R (reorth only)
+  double* s = dyn + 2 * RT;       // n_c
   if (a.n_c) {
     if (a.n_c <= NC_INLINE) {
       // s_i = sum_k Ginv[i,k] u_k, fixed order (every CTA computes the same s)
@@ -381,6 +385,7 @@ colreduce_kernel(const IterArgs* __restrict__ ap) {
 // ---------------------------------------------------------------------------
 // K5: beta, w_{j+1} = z + beta w_j  (- W c' with c' = (AW^T w)/diag)
 
+template <int RPT>
 __global__ void __launch_bounds__(kThreads)
 wupdate_kernel(const IterArgs* __restrict__ ap) {
   const IterArgs& a = *ap;
@@ -402,10 +407,10 @@ wupdate_kernel(const IterArgs* __restrict__ ap) {
   __shared__ bool s_last;
   const int S = gridDim.y;           // column splits (small n: rows alone do not fill the GPU)
   const int split = blockIdx.y;
-  const int64_t r0 = (int64_t)blockIdx.x * (kThreads * WU_RPT);
-  double acc[WU_RPT];
+  const int64_t r0 = (int64_t)blockIdx.x * (kThreads * RPT);
+  double acc[RPT];
 #pragma unroll
-  for (int q = 0; q < WU_RPT; ++q) acc[q] = 0.0;
+  for (int q = 0; q < RPT; ++q) acc[q] = 0.0;
   if (a.reorth) {
     const long long kb = (j + 1) * split / S, ke = (j + 1) * (split + 1) / S;
     const double* red = a.sums + a.rz_off + 1;
@@ -423,7 +428,7 @@ wupdate_kernel(const IterArgs* __restrict__ ap) {
         const double* col = a.W.at(k0 + k) + r0 + threadIdx.x;
         const double ck = cp[k];
 #pragma unroll
-        for (int q = 0; q < WU_RPT; ++q)
+        for (int q = 0; q < RPT; ++q)
           if (r0 + threadIdx.x + q * kThreads < a.n) acc[q] += col[q * kThreads] * ck;
       }
     }
@@ -433,7 +438,7 @@ wupdate_kernel(const IterArgs* __restrict__ ap) {
     // park this split's partial sums; the last split of the row block adds
     // them in split order (deterministic) and finishes the rows
 #pragma unroll
-    for (int q = 0; q < WU_RPT; ++q) {
+    for (int q = 0; q < RPT; ++q) {
       const int64_t i = r0 + threadIdx.x + q * kThreads;
       if (i < a.n) a.part_wu[(int64_t)split * a.n + i] = acc[q];
     }
@@ -450,7 +455,7 @@ wupdate_kernel(const IterArgs* __restrict__ ap) {
     if (finisher) {
       __threadfence();
 #pragma unroll
-      for (int q = 0; q < WU_RPT; ++q) {
+      for (int q = 0; q < RPT; ++q) {
         const int64_t i = r0 + threadIdx.x + q * kThreads;
         double t = 0.0;
         if (i < a.n)
@@ -464,7 +469,7 @@ wupdate_kernel(const IterArgs* __restrict__ ap) {
     const double* wo = a.W.at(j);
     double* wn = a.W.at(j + 1);
 #pragma unroll
-    for (int q = 0; q < WU_RPT; ++q) {
+    for (int q = 0; q < RPT; ++q) {
       const int64_t i = r0 + threadIdx.x + q * kThreads;
       if (i < a.n) {
         double v = __dadd_rn(z[i], __dmul_rn(beta, wo[i]));   // w = z + beta w
@@ -618,6 +623,8 @@ using namespace rcg;
 struct rcg_trace {
   rcg_trace_view view{};
   std::vector<std::pair<void*, size_t>> allocs;   // returned to the pool on free
+  std::vector<rcg::VmmBuf> vbufs;                  // Krylov histories (VA ranges)
+  std::shared_ptr<rcg::VmmPool> vpool;
   std::shared_ptr<rcg::Pool> pool;
   cudaStream_t stream = nullptr;
   int device = 0;
@@ -637,6 +644,10 @@ extern "C" void rcg_trace_free(rcg_trace* t) {
   cudaStreamSynchronize(t->stream);
   for (auto& pb : t->allocs)
     if (pb.first) t->pool->put(pb.first, pb.second);
+  for (auto& vb : t->vbufs) {
+    if (t->vpool) t->vpool->give(vb);
+    else vb.release();
+  }
   cudaSetDevice(prev);
   delete t;
 }
@@ -676,6 +687,53 @@ int grow(Ctx* c, Grow& g, int64_t need_cols, int64_t ld, int64_t used_cols) {
   return RCG_OK;
 }
 
+// Krylov history on a growable VA range: the pointer never moves, growth
+// maps more physical chunks (no copy, no peak)
+struct Hist {
+  VmmBuf v;
+  double* ptr = nullptr;
+  int64_t cols = 0;
+};
+
+int hist_init(Ctx* c, Hist& h, int64_t max_cols, int64_t init_cols, int64_t ld) {
+  size_t total = 0, free_b = 0;
+  cudaMemGetInfo(&free_b, &total);
+  const size_t col_bytes = sizeof(double) * (size_t)ld;
+  size_t max_bytes = std::min((size_t)std::max<int64_t>(max_cols, 1) * col_bytes, total);
+  const size_t chunk = std::min<size_t>(std::max<size_t>(64 * col_bytes, (size_t)2 << 20), (size_t)512 << 20);
+  const size_t g = vmm_granularity(c->device);
+  const size_t chunk_r = std::max(g, ((chunk + g - 1) / g) * g);
+  const size_t reserved = ((std::max<size_t>(max_bytes, 1) + chunk_r - 1) / chunk_r) * chunk_r;
+  if (!c->vpool->take(chunk_r, reserved, &h.v) && !h.v.reserve(c->chunks, c->device, max_bytes, chunk))
+    return set_error(c, RCG_ERR_OOM, "cannot reserve %.2f GB of device address space", max_bytes / 1e9);
+  h.ptr = h.v.ptr();
+  const size_t want = std::min(max_bytes, (size_t)init_cols * col_bytes);
+  if (!h.v.ensure(want)) {
+    c->vpool->clear();  // idle histories of earlier solves, then retry once
+    c->chunks->trim();
+    if (!h.v.ensure(want))
+      return set_error(c, RCG_ERR_OOM, "out of device memory for a Krylov history (%lld columns, %.2f GB)",
+                       (long long)init_cols, init_cols * col_bytes / 1e9);
+  }
+  h.cols = (int64_t)(h.v.mapped / col_bytes);
+  return RCG_OK;
+}
+
+int hist_grow(Ctx* c, Hist& h, int64_t need_cols, int64_t ld) {
+  if (need_cols <= h.cols) return RCG_OK;
+  const size_t col_bytes = sizeof(double) * (size_t)ld;
+  const size_t want = (size_t)std::max<int64_t>(need_cols, h.cols + h.cols / 4) * col_bytes;
+  if (!h.v.ensure(std::min(want, h.v.reserved)) && !h.v.ensure((size_t)need_cols * col_bytes)) {
+    c->vpool->clear();
+    c->chunks->trim();
+    if (!h.v.ensure((size_t)need_cols * col_bytes))
+      return set_error(c, RCG_ERR_OOM, "out of device memory growing a Krylov history to %lld columns (%.2f GB)",
+                       (long long)need_cols, need_cols * col_bytes / 1e9);
+  }
+  h.cols = (int64_t)(h.v.mapped / col_bytes);
+  return RCG_OK;
+}
+
 }  // namespace
 
 // collectives only for sharded calls (a context may own a communicator and
@@ -708,10 +766,13 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   T->stream = c->stream;
   T->device = c->device;
   T->pool = c->pool;
-  Grow gW, gAW, gZ, gR, gPR, gSum;
+  T->vpool = c->vpool;
+  Grow gPR, gSum;
+  Hist gW, gAW, gZ, gR;
   auto fail = [&](int rc) {
-    for (Grow* g : {&gW, &gAW, &gZ, &gR, &gPR, &gSum})
+    for (Grow* g : {&gPR, &gSum})
       if (g->ptr) c->pool->put(g->ptr, g->bytes);
+    for (Hist* h : {&gW, &gAW, &gZ, &gR}) c->vpool->give(h->v);
     rcg_trace_free(T);
     return rc;
   };
@@ -723,15 +784,28 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     return RCG_OK;
   };
 
-  const int R = rows_per_block_for(c, n);
+  // row tiles: K3 needs 2 smem tiles only when reorthogonalizing and K2 one
+  // only with an augmentation basis; otherwise tiles grow so the grid stays
+  // at <= 8 CTAs/SM (few last-block arrivals even at n = 16.7 M)
+  auto big_tile = [&](int R0) {
+    const int64_t rmin = ceil_div(ceil_div(n, (int64_t)8 * c->num_sms), kThreads) * kThreads;
+    return (int)std::max<int64_t>(R0, rmin);
+  };
+  const int R = reorth ? rows_per_block_for(c, n) : big_tile(rows_per_block_for(c, n));
   const int nb = (int)std::max<int64_t>(1, ceil_div(n, R));
   static const int upd_tiles = env_int("RCG_UPD_TILES_PER_SM", 8);
-  const int Ru = rows_per_block_for(c, n, upd_tiles);
+  const int Ru = n_c ? rows_per_block_for(c, n, upd_tiles) : big_tile(rows_per_block_for(c, n, upd_tiles));
   const int nbu = (int)std::max<int64_t>(1, ceil_div(n, Ru));
   const int nbs = spmv_partials(c, A);
   // K3 column splits for small n (the AW GEMV-T otherwise runs on nb CTAs only)
   const int pre_split = reorth ? (int)std::max<int64_t>(1, std::min<int64_t>(8, (2 * c->num_sms) / nb)) : 1;
-  const int wu_grid = (int)std::max<int64_t>(1, ceil_div(n, (int64_t)kThreads * WU_RPT));
+  // K5 rows per thread: 4, or 16 when that keeps the grid below 8 CTAs/SM
+  // (n ~ 1e7: fewer last-block arrivals on one counter)
+  const int wu_rpt = ceil_div(n, (int64_t)kThreads * WU_RPT) > 8 * c->num_sms ? 16 : WU_RPT;
+  const int wu_grid = (int)std::max<int64_t>(1, ceil_div(n, (int64_t)kThreads * wu_rpt));
+  // launch grids: the tile kernels grid-stride, capped at a few CTAs per SM
+  const int cap_grid = 8 * c->num_sms;
+  const int nb_l = nb, nbu_l = nbu, wu_l = std::min(wu_grid, cap_grid);
   // K5 column splits when the row blocks alone cannot fill the SMs (small n)
   const int wu_split = reorth ? (int)std::max<int64_t>(1, std::min<int64_t>(16, (2 * c->num_sms) / wu_grid)) : 1;
 
@@ -771,10 +845,15 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     if (h != c->m_hint.end()) hint = std::max<int64_t>(64, h->second + h->second / 8 + 16);
   }
   const int64_t init_cols = std::min<int64_t>(max_it + 2, hint);
-  if ((rc = grow(c, gW, storeW ? init_cols : 2, ld, 0))) return fail(rc);
-  if ((rc = grow(c, gAW, reorth ? init_cols : 1, ld, 0))) return fail(rc);
-  if ((rc = grow(c, gZ, capture ? init_cols : 2, ld, 0))) return fail(rc);
-  if (store && (rc = grow(c, gR, init_cols, ld, 0))) return fail(rc);
+  const int64_t full_cols = max_it + 2;
+  // capped z history: columns 0..cap-1 kept, column cap is the scratch column
+  const int64_t zcap = (capture && cfg->krylov_cap > 0 && cfg->krylov_cap < max_it + 1) ? cfg->krylov_cap : 0;
+  if ((rc = hist_init(c, gW, storeW ? full_cols : 2, storeW ? init_cols : 2, ld))) return fail(rc);
+  if ((rc = hist_init(c, gAW, reorth ? full_cols : 1, reorth ? init_cols : 1, ld))) return fail(rc);
+  if ((rc = hist_init(c, gZ, capture ? (zcap ? zcap + 1 : full_cols) : 2,
+                      capture ? (zcap ? zcap + 1 : init_cols) : 2, ld)))
+    return fail(rc);
+  if (store && (rc = hist_init(c, gR, full_cols, init_cols, ld))) return fail(rc);
 
   auto reo_cols = [&]() { return gAW.cols; };
   auto ensure_sums = [&](void) -> int {
@@ -827,7 +906,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     a.r = r;
     a.W = colsel(gW.ptr, ld, storeW ? 0 : 2);
     a.AW = colsel(gAW.ptr, ld, reorth ? 0 : 1);
-    a.Z = colsel(gZ.ptr, ld, capture ? 0 : 2);
+    a.Z = colsel(gZ.ptr, ld, capture ? 0 : 2, 0, zcap);
     a.R = colsel(store ? gR.ptr : nullptr, ld, 0);
     a.waw_diag = wawd;
     a.alphas = alphas;
@@ -847,6 +926,8 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     a.rows_per_block = R;
     a.rows_per_block_upd = Ru;
     a.nb_pre = nb;
+    a.nb_upd = nbu;
+    a.nb_wu = wu_grid;
     spmv_args_fill(A, &a.spmv);
     a.spmv.xs = a.W;
     a.spmv.ys = a.AW;
@@ -864,7 +945,8 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   // systems of a sequence (n_c changes from system to system)
   const int64_t nc_bucket = ((n_c + 1 + 63) / 64) * 64;
   const size_t smem_upd = sizeof(double) * (n_c ? Ru : 1);
-  const size_t smem_pre = sizeof(double) * (2 * (size_t)R + nc_bucket);
+  // z / w_j tiles only when reorthogonalizing (they feed the AW GEMV-T)
+  const size_t smem_pre = sizeof(double) * ((reorth ? 2 * (size_t)R : 0) + nc_bucket);
   RCG_CUDA(c, cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(smem_upd, 1024)));
   static const int pre_cg = env_int("RCG_PRE_CG", 8);
@@ -918,10 +1000,10 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     T->view.AW = reorth ? gAW.ptr : nullptr;
     T->view.R = store ? gR.ptr : nullptr;
     T->view.waw = wawd;
-    T->allocs.emplace_back(gW.ptr, gW.bytes);
-    T->allocs.emplace_back(gAW.ptr, gAW.bytes);
-    T->allocs.emplace_back(gZ.ptr, gZ.bytes);
-    T->allocs.emplace_back(gR.ptr, gR.bytes);
+    for (Hist* h : {&gW, &gAW, &gZ, &gR}) {
+      if (h->v.base) T->vbufs.push_back(h->v);
+      h->v = VmmBuf();
+    }
     T->allocs.emplace_back(gPR.ptr, gPR.bytes);
     T->allocs.emplace_back(gSum.ptr, gSum.bytes);
     gW.ptr = gAW.ptr = gZ.ptr = gR.ptr = gPR.ptr = gSum.ptr = nullptr;
@@ -948,11 +1030,11 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   };
 
   // ---- z0, rz0, w0 (solver.py:221-231) ----
-  update_kernel<<<nbu, kThreads, smem_upd, c->stream>>>(dargs, 1);
+  update_kernel<<<nbu_l, kThreads, smem_upd, c->stream>>>(dargs, 1);
   RCG_LAUNCH_CHECK(c);
   if ((rc = allreduce_h(H, c, gSum.ptr + 1, (size_t)(1 + n_c)))) return fail(rc);
   if ((rc = launch_coarse(1))) return fail(rc);
-  pre<<<nb, kThreads, smem_pre, c->stream>>>(dargs, 1);
+  pre<<<nb_l, kThreads, smem_pre, c->stream>>>(dargs, 1);
   RCG_LAUNCH_CHECK(c);
   if ((rc = allreduce_h(H, c, gSum.ptr + a.rz_off, 1))) return fail(rc);
   init_finish_kernel<<<1, 1, 0, c->stream>>>(dargs);
@@ -992,7 +1074,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
       if (direct) prof_end(c);
       if ((rc2 = allreduce_h(H, c, gSum.ptr, 1))) return rc2;
       if (direct) prof_begin(c, RCG_K_UPDATE, 8.0 * nd * (6 + jac + n_c + (store ? 1 : 0)));
-      update_kernel<<<nbu, kThreads, smem_upd, c->stream>>>(dargs, 0);
+      update_kernel<<<nbu_l, kThreads, smem_upd, c->stream>>>(dargs, 0);
       RCG_LAUNCH_CHECK(c);
       if (direct) prof_end(c);
       if ((rc2 = allreduce_h(H, c, gSum.ptr + 1, (size_t)(1 + n_c)))) return rc2;
@@ -1002,7 +1084,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
         if (direct) prof_end(c);
       }
       if (direct) prof_begin(c, RCG_K_PRECOND, 8.0 * nd * (2 + jac + n_c + (reorth ? 1.0 + js : 0.0)));
-      pre<<<dim3(nb, pre_split), kThreads, smem_pre, c->stream>>>(dargs, 0);
+      pre<<<dim3(nb_l, pre_split), kThreads, smem_pre, c->stream>>>(dargs, 0);
       RCG_LAUNCH_CHECK(c);
       if (direct) prof_end(c);
       if (reorth) {
@@ -1014,7 +1096,10 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
       // one packed allreduce: (r, z) and the 2(j+1) reorth dot products
       if ((rc2 = allreduce_h(H, c, gSum.ptr + a.rz_off, (size_t)(1 + (reorth ? 2 * (jj + 1) : 0))))) return rc2;
       if (direct) prof_begin(c, RCG_K_WUPDATE, 8.0 * nd * (3 + (reorth ? js : 0.0)));
-      wupdate_kernel<<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
+      if (wu_rpt == 16)
+        wupdate_kernel<16><<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
+      else
+        wupdate_kernel<WU_RPT><<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
       RCG_LAUNCH_CHECK(c);
       if (direct) prof_end(c);
     }
@@ -1027,19 +1112,19 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     const int64_t need = it + B + 2;
     bool regrown = false;
     if (storeW && need > gW.cols) {
-      if ((rc = grow(c, gW, need, ld, it + 1))) return fail(rc);
+      if ((rc = hist_grow(c, gW, need, ld))) return fail(rc);
       regrown = true;
     }
     if (reorth && need > gAW.cols) {
-      if ((rc = grow(c, gAW, need, ld, it + 1))) return fail(rc);
+      if ((rc = hist_grow(c, gAW, need, ld))) return fail(rc);
       regrown = true;
     }
-    if (capture && need > gZ.cols) {
-      if ((rc = grow(c, gZ, need, ld, it + 1))) return fail(rc);
+    if (capture && !zcap && need > gZ.cols) {
+      if ((rc = hist_grow(c, gZ, need, ld))) return fail(rc);
       regrown = true;
     }
     if (store && need > gR.cols) {
-      if ((rc = grow(c, gR, need, ld, it + 1))) return fail(rc);
+      if ((rc = hist_grow(c, gR, need, ld))) return fail(rc);
       regrown = true;
     }
     if (regrown) {

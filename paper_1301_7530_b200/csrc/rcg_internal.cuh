@@ -35,7 +35,9 @@ struct Pool {
   void trim();
 };
 
-struct Comm;  // comm.cu
+struct Comm;       // comm.cu
+struct ChunkPool;  // vmm.cuh
+struct VmmPool;    // vmm.cuh
 
 // ---------------------------------------------------------------------------
 // context
@@ -64,6 +66,8 @@ struct Ctx {
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
   std::shared_ptr<Pool> pool = std::make_shared<Pool>();
+  std::shared_ptr<ChunkPool> chunks;     // physical chunks of the VA-range histories
+  std::shared_ptr<VmmPool> vpool;        // whole mapped history ranges kept across solves
   std::map<int64_t, int64_t> m_hint;     // n -> iterations of the last solve
   Comm* comm = nullptr;                  // NCCL communicator (sharded runs)
   void* dargs = nullptr;                 // device-resident solve arguments (graph replay)
@@ -164,24 +168,30 @@ __host__ __device__ __forceinline__ int64_t pad_ld(int64_t n) { return ceil_div(
 
 // A column of a column-major history buffer chosen by the device-side
 // iteration counter: column (j + shift) (mod `mod` when mod > 0).
+// (clamp > 0: columns >= clamp all map to column `clamp`, a scratch column
+// past a capped history)
 struct ColSel {
   double* base;
   int64_t ld;
   int64_t mod;
   int64_t shift;
+  int64_t clamp;
   __device__ __forceinline__ double* at(long long j) const {
     long long c = j + shift;
     if (mod > 0) c %= mod;
+    if (clamp > 0 && c > clamp) c = clamp;
     return base + (int64_t)c * ld;
   }
 };
 
-__host__ __forceinline__ ColSel colsel(double* base, int64_t ld = 0, int64_t mod = 1, int64_t shift = 0) {
+__host__ __forceinline__ ColSel colsel(double* base, int64_t ld = 0, int64_t mod = 1, int64_t shift = 0,
+                                       int64_t clamp = 0) {
   ColSel s;
   s.base = base;
   s.ld = ld;
   s.mod = mod;
   s.shift = shift;
+  s.clamp = clamp;
   return s;
 }
 

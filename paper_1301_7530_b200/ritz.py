@@ -124,7 +124,7 @@ def ritz_vectors_device(trace, values_desc_dev, idx, scale_by_theta):
     """(k, ld) device block: y_i = V q_{idx_i} (/ sqrt|theta_i|) — the skinny
     Z @ Qtilde GEMM over the device z history (``rcg_ritz_vectors``)."""
     torch = _torch()
-    m = trace.iterations
+    m = trace.extraction_length()
     Z, ld, n = trace.device_z()
     a, b, rz = trace.device_coefficients()
     idx_d = torch.as_tensor(np.asarray(idx, dtype=np.int64)).to("cuda")

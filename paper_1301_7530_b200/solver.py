@@ -260,12 +260,17 @@ class SolveConfig:
     reorthogonalize: bool = True
     trace_capture: bool = True
     store_directions: bool = False
+    # extension (not in the reference): keep only z_0..z_{cap-1}; Ritz
+    # extraction then uses the leading cap x cap Lanczos block
+    krylov_cap: int | None = None
 
     def __post_init__(self):
         if not 0.0 < self.tol < 1.0:
             raise ContractViolation("tol must be in (0, 1)")
         if self.max_iters < 1:
             raise ContractViolation("max_iters must be >= 1")
+        if self.krylov_cap is not None and self.krylov_cap < 1:
+            raise ContractViolation("krylov_cap must be >= 1")
 
 
 class _TraceOwner:
@@ -362,6 +367,7 @@ class SolveTrace:
     # device-side handles (not part of the reference dataclass contract)
     _owner: object = field(default=None, repr=False, compare=False)
     device_seconds: float = field(default=0.0, repr=False, compare=False)
+    krylov_cap: object = field(default=None, repr=False, compare=False)
     b_norm: float = field(default=0.0, repr=False, compare=False)
 
     def to_json_dict(self, spectrum=None, eps_cg=None):
@@ -392,13 +398,20 @@ class SolveTrace:
             converged=bool(d.get("converged", False)),
         )
 
+    def extraction_length(self):
+        """m used for Ritz extraction: the full m, or the leading block kept
+        under the krylov_cap extension (exact Lanczos on H_cap)."""
+        if self.krylov_cap and len(self.z_history) < self.iterations:
+            return len(self.z_history)
+        return self.iterations
+
     # -- device access used by the Ritz path -----------------------------
     def device_coefficients(self):
         """(alphas, betas, rz) as device tensors of length >= m."""
         torch = _torch()
-        m = self.iterations
+        m = self.extraction_length()
         v = self._owner.view if self._owner is not None else None
-        if v is not None and len(self.alphas) == m:
+        if v is not None and len(self.alphas) >= m:
             def wrap(p, count):
                 arr = _lib.CudaArray(self._owner, p, (max(count, 1),), (1,))
                 return torch.as_tensor(arr, device="cuda")
@@ -412,7 +425,7 @@ class SolveTrace:
         """(m, ld) device tensor of z_0..z_{m-1} and its ld, uploading a host
         z_history (e.g. a trace read from JSON) when needed."""
         torch = _torch()
-        m = self.iterations
+        m = self.extraction_length()
         zh = self.z_history
         if isinstance(zh, DeviceColumns) and zh.device() is not None and len(zh) >= m:
             t = zh.device()
@@ -453,7 +466,8 @@ def apcg_solve(A: SparseSpdMatrix, M: Preconditioner, D: DeflationOperator, b, c
     h = A.device_csr()
     inv = M.device_inv_diag() if M is not None else None
     scfg = _lib.RcgSolveCfg(float(cfg.tol), int(cfg.max_iters), int(bool(cfg.reorthogonalize)),
-                            int(bool(cfg.trace_capture)), int(bool(cfg.store_directions)), 0)
+                            int(bool(cfg.trace_capture)), int(bool(cfg.store_directions)), 0,
+                            int(getattr(cfg, "krylov_cap", None) or 0))
     th = _lib.C.c_void_p()
     t0 = time.perf_counter()
     if hasattr(A, "plan"):
@@ -491,8 +505,11 @@ def apcg_solve(A: SparseSpdMatrix, M: Preconditioner, D: DeflationOperator, b, c
     else:
         trace.residual_norms = [float(view.r0_norm)]
     ld = int(view.ld)
+    cap = getattr(cfg, "krylov_cap", None)
     if cfg.trace_capture:
-        trace.z_history = _history(owner, view.Z, ld, m, A.n, cap_cols=m + 1)
+        mz = min(m, cap) if cap else m
+        trace.z_history = _history(owner, view.Z, ld, mz, A.n, cap_cols=mz + 1)
+        trace.krylov_cap = cap
     if cfg.store_directions:
         trace.w_history = _history(owner, view.W, ld, m, A.n, cap_cols=m + 1)
         trace.r_history = _history(owner, view.R, ld, m, A.n, cap_cols=m + 1)

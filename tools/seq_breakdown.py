@@ -23,16 +23,18 @@ for rep_i in range(2):
         torch.cuda.synchronize(); t2 = time.perf_counter()
         x, tr = rcg.apcg_solve(A, M, D, b, cfg)
         t3 = time.perf_counter()
+        dev_s = tr.device_seconds
         spec = rcg.select_spectrum(tr, strat)
         torch.cuda.synchronize(); t4 = time.perf_counter()
         rcg.update_basis_srks(state, spec, k)
         torch.cuda.synchronize(); t5 = time.perf_counter()
         if state.n_c >= 61:
             state.restart()
-        del tr, x
+        m, nsel = spec.m, int(spec.converged_mask.sum())
+        del tr, x, spec
         torch.cuda.synchronize(); t6 = time.perf_counter()
         if rep_i == 1:
-            print(f"k={k} m={spec.m} nc={D.n_c} build={1e3*(t2-t1):.1f}ms solve_wall={1e3*(t3-t2):.1f}ms "
-                  f"select={1e3*(t4-t3):.1f}ms ritzvec={1e3*(t5-t4):.1f}ms free={1e3*(t6-t5):.1f}ms sel={int(spec.converged_mask.sum())}")
+            print(f"k={k} m={m} nc={D.n_c} build={1e3*(t2-t1):.1f}ms solve_wall={1e3*(t3-t2):.1f}ms dev={1e3*dev_s:.1f}ms "
+                  f"select={1e3*(t4-t3):.1f}ms ritzvec={1e3*(t5-t4):.1f}ms free={1e3*(t6-t5):.1f}ms sel={nsel}")
     torch.cuda.synchronize()
     print("total", time.perf_counter() - t0)
