@@ -801,7 +801,8 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   const int pre_split = reorth ? (int)std::max<int64_t>(1, std::min<int64_t>(8, (2 * c->num_sms) / nb)) : 1;
   // K5 rows per thread: 4, or 16 when that keeps the grid below 8 CTAs/SM
   // (n ~ 1e7: fewer last-block arrivals on one counter)
-  const int wu_rpt = ceil_div(n, (int64_t)kThreads * WU_RPT) > 8 * c->num_sms ? 16 : WU_RPT;
+  // (without reorth only: the 16-row variant is slow on the W GEMV)
+  const int wu_rpt = (!reorth && ceil_div(n, (int64_t)kThreads * WU_RPT) > 8 * c->num_sms) ? 16 : WU_RPT;
   const int wu_grid = (int)std::max<int64_t>(1, ceil_div(n, (int64_t)kThreads * wu_rpt));
   // launch grids: the tile kernels grid-stride, capped at a few CTAs per SM
   const int cap_grid = 8 * c->num_sms;

@@ -45,6 +45,7 @@ strat = rcg.RecycleStrategy("srks", epsilon=eps, nc_limit=ncl)
 for A, _ in dev:
     A.device_csr()
 ctx = _lib.context()
+rcg.run_sequence(iter(dev[:2]), rcg.Preconditioner.jacobi, strat, cfg)   # warm-up: graphs, pools
 ctx.reset_stats()
 ctx.set_profiling(True)
 torch.cuda.synchronize()
