@@ -173,6 +173,12 @@ int rcg_comm_init(rcg_ctx* ctx, const char* nccl_lib, const void* id_host, int n
 int rcg_comm_destroy(rcg_ctx* ctx);
 int rcg_allreduce_sum(rcg_ctx* ctx, double* buf, int64_t count);
 int rcg_halo_exchange(rcg_ctx* ctx, const rcg_halo* halo, double* vec);
+/* Single-process loopback transport (validation of the sharded path on one
+ * GPU): `nranks` host threads, each with its own context and stream, act as
+ * ranks; collectives use device copies ordered by CUDA events. */
+int rcg_loop_group_create(int nranks, void** group_out_host);
+void rcg_loop_group_destroy(void* group);
+int rcg_comm_init_loopback(rcg_ctx* ctx, void* group, int rank);
 
 /* ---- operators (core.py) ------------------------------------------------- */
 /* y = A x  (spmv, core.py:114-119 / SparseSpdMatrix.__matmul__ core.py:110-111) */

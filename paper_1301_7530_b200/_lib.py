@@ -86,6 +86,9 @@ SIGNATURES = {
     "rcg_comm_destroy": (C.c_int, [_vp]),
     "rcg_allreduce_sum": (C.c_int, [_vp, _vp, _i64]),
     "rcg_halo_exchange": (C.c_int, [_vp, C.POINTER(RcgHalo), _vp]),
+    "rcg_loop_group_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
+    "rcg_loop_group_destroy": (None, [_vp]),
+    "rcg_comm_init_loopback": (C.c_int, [_vp, _vp, C.c_int]),
     "rcg_spmv": (C.c_int, [_vp, C.POINTER(RcgCsr), _vp, _vp]),
     "rcg_spmm": (C.c_int, [_vp, C.POINTER(RcgCsr), _vp, _i64, _i64, _vp, _i64]),
     "rcg_csr_diagonal": (C.c_int, [_vp, C.POINTER(RcgCsr), _vp, _vp]),

@@ -9,6 +9,9 @@
 
 #include <dlfcn.h>
 #include <cstring>
+#include <condition_variable>
+#include <mutex>
+#include <vector>
 
 namespace rcg {
 
@@ -33,11 +36,45 @@ struct Nccl {
   const char* (*errStr)(ncclResult_t) = nullptr;
 };
 
+// Single-process loopback transport (validation of the sharded path on one
+// GPU): ranks are host threads with their own streams on the same device.
+// Collectives exchange data with device copies ordered by CUDA events;
+// a host barrier per collective guarantees every event a stream waits on has
+// already been recorded, so all dependencies point to enqueued work (no
+// kernel ever spins on another rank).
+struct LoopGroup {
+  int nranks = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long generation = 0;
+  // per rank, two slot sets (round parity) for allreduce / halo staging
+  std::vector<double*> slot[2];
+  std::vector<size_t> slot_cap[2];
+  std::vector<cudaEvent_t> ready[2];     // slot written (recorded by its owner)
+  std::vector<cudaEvent_t> consumed[2];  // owner's consumption of everyone's slots done
+  std::vector<const rcg_halo*> halo;     // halo plan of each rank (current exchange)
+  std::vector<double*> send_buf;         // each rank's packed send buffer (current exchange)
+  long long round[64] = {0};
+  void barrier() {
+    std::unique_lock<std::mutex> l(mu);
+    const long long gen = generation;
+    if (++arrived == nranks) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(l, [&] { return generation != gen; });
+    }
+  }
+};
+
 struct Comm {
   Nccl api;
   ncclComm_t comm = nullptr;
   int nranks = 1;
   int rank = 0;
+  LoopGroup* loop = nullptr;
 };
 
 static int load_nccl(const char* path, Nccl* n, std::string* err) {
@@ -77,8 +114,72 @@ static int load_nccl(const char* path, Nccl* n, std::string* err) {
 
 int comm_ranks(const Ctx* c) { return c->comm ? c->comm->nranks : 1; }
 
+__global__ void sum_slots_kernel(double* out, double* const* slots, int nranks, size_t count) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < nranks; ++r) s += slots[r][i];   // rank order: identical bits on every rank
+    out[i] = s;
+  }
+}
+
+static int loop_allreduce(Ctx* c, double* buf, size_t count) {
+  LoopGroup* g = c->comm->loop;
+  const int me = c->comm->rank, R = g->nranks;
+  const int par = (int)(g->round[me] & 1);
+  ++g->round[me];
+  // my slot of this parity was last read two rounds ago: wait for every rank's consumption
+  for (int q = 0; q < R; ++q) RCG_CUDA(c, cudaStreamWaitEvent(c->stream, g->consumed[par][q], 0));
+  if (g->slot_cap[par][me] < count) {
+    // grow (all ranks are past the previous use of this parity, see the wait above)
+    RCG_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (g->slot[par][me]) cudaFree(g->slot[par][me]);
+    RCG_CUDA(c, cudaMalloc(&g->slot[par][me], std::max<size_t>(count, 4096) * sizeof(double)));
+    g->slot_cap[par][me] = std::max<size_t>(count, 4096);
+  }
+  RCG_CUDA(c, cudaMemcpyAsync(g->slot[par][me], buf, count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  RCG_CUDA(c, cudaEventRecord(g->ready[par][me], c->stream));
+  g->barrier();  // every rank's slot copy + event is enqueued
+  for (int q = 0; q < R; ++q)
+    if (q != me) RCG_CUDA(c, cudaStreamWaitEvent(c->stream, g->ready[par][q], 0));
+  double** dptrs = nullptr;
+  RCG_CUDA(c, cudaMallocAsync((void**)&dptrs, sizeof(double*) * R, c->stream));
+  std::vector<double*> hp(g->slot[par].begin(), g->slot[par].end());
+  RCG_CUDA(c, cudaMemcpyAsync(dptrs, hp.data(), sizeof(double*) * R, cudaMemcpyHostToDevice, c->stream));
+  sum_slots_kernel<<<(unsigned)std::min<size_t>((count + 255) / 256, 64), 256, 0, c->stream>>>(buf, dptrs, R, count);
+  RCG_LAUNCH_CHECK(c);
+  RCG_CUDA(c, cudaStreamSynchronize(c->stream));  // hp / dptrs lifetime (validation transport: simplicity first)
+  cudaFreeAsync(dptrs, c->stream);
+  RCG_CUDA(c, cudaEventRecord(g->consumed[par][me], c->stream));
+  g->barrier();  // consumption events recorded before anyone reuses this parity
+  return RCG_OK;
+}
+
+static int loop_halo(Ctx* c, const rcg_halo* H, double* dst_col) {
+  LoopGroup* g = c->comm->loop;
+  const int me = c->comm->rank, R = g->nranks;
+  const int par = (int)(g->round[me] & 1);
+  ++g->round[me];
+  g->halo[me] = H;
+  g->send_buf[me] = H->send_buf;
+  RCG_CUDA(c, cudaEventRecord(g->ready[par][me], c->stream));   // after the pack kernel
+  g->barrier();
+  for (int q = 0; q < R; ++q) {
+    if (q == me) continue;
+    const rcg_halo* Hq = g->halo[q];
+    const int64_t nr = H->recv_off[q + 1] - H->recv_off[q];
+    if (nr <= 0) continue;
+    RCG_CUDA(c, cudaStreamWaitEvent(c->stream, g->ready[par][q], 0));
+    RCG_CUDA(c, cudaMemcpyAsync(dst_col + H->n_local + H->recv_off[q], g->send_buf[q] + Hq->send_off[me],
+                                nr * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  }
+  RCG_CUDA(c, cudaEventRecord(g->consumed[par][me], c->stream));
+  g->barrier();
+  return RCG_OK;
+}
+
 int allreduce_sum(Ctx* c, double* buf, size_t count) {
   if (!c->comm || c->comm->nranks <= 1 || count == 0) return RCG_OK;
+  if (c->comm->loop) return loop_allreduce(c, buf, count);
   RCG_NCCL(c, c->comm->api.allReduce(buf, buf, count, kNcclFloat64, kNcclSum, c->comm->comm, c->stream));
   return RCG_OK;
 }
@@ -94,6 +195,13 @@ __global__ void halo_pack_kernel(int64_t total, const int32_t* __restrict__ idx,
 
 int halo_exchange(Ctx* c, const rcg_halo* H, ColSel src, const SolveState* st, double* dst_col) {
   if (!H || !c->comm || c->comm->nranks <= 1) return RCG_OK;
+  if (c->comm->loop) {
+    // loopback: the single send buffer may be repacked only after every rank
+    // consumed the previous exchange (events recorded before the last barrier)
+    LoopGroup* g = c->comm->loop;
+    for (int p = 0; p < 2; ++p)
+      for (int q = 0; q < g->nranks; ++q) RCG_CUDA(c, cudaStreamWaitEvent(c->stream, g->consumed[p][q], 0));
+  }
   const int64_t total = H->send_off[H->nranks];
   if (total > 0) {
     int64_t g = ceil_div(total, kThreads);
@@ -101,6 +209,7 @@ int halo_exchange(Ctx* c, const rcg_halo* H, ColSel src, const SolveState* st, d
     halo_pack_kernel<<<(unsigned)g, kThreads, 0, c->stream>>>(total, H->send_idx, src, st, H->send_buf);
     RCG_LAUNCH_CHECK(c);
   }
+  if (c->comm->loop) return loop_halo(c, H, dst_col);
   Nccl& api = c->comm->api;
   RCG_NCCL(c, api.groupStart());
   for (int q = 0; q < H->nranks; ++q) {
@@ -118,7 +227,7 @@ int halo_exchange(Ctx* c, const rcg_halo* H, ColSel src, const SolveState* st, d
 
 void comm_free(Ctx* c) {
   if (c->comm) {
-    if (c->comm->comm && c->comm->api.commDestroy) c->comm->api.commDestroy(c->comm->comm);
+    if (!c->comm->loop && c->comm->comm && c->comm->api.commDestroy) c->comm->api.commDestroy(c->comm->comm);
     delete c->comm;
     c->comm = nullptr;
   }
@@ -180,4 +289,51 @@ extern "C" int rcg_allreduce_sum(rcg_ctx* ctx, double* buf, int64_t count) {
 extern "C" int rcg_halo_exchange(rcg_ctx* ctx, const rcg_halo* H, double* vec) {
   if (!ctx || !H) return RCG_ERR_CONTRACT;
   return halo_exchange(ctx, H, colsel(vec), nullptr, vec);
+}
+
+extern "C" int rcg_loop_group_create(int nranks, void** out) {
+  if (!out || nranks < 1 || nranks > 64) return RCG_ERR_CONTRACT;
+  LoopGroup* g = new LoopGroup();
+  g->nranks = nranks;
+  for (int p = 0; p < 2; ++p) {
+    g->slot[p].assign(nranks, nullptr);
+    g->slot_cap[p].assign(nranks, 0);
+    g->ready[p].resize(nranks);
+    g->consumed[p].resize(nranks);
+    for (int r = 0; r < nranks; ++r) {
+      cudaEventCreateWithFlags(&g->ready[p][r], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&g->consumed[p][r], cudaEventDisableTiming);
+      cudaEventRecord(g->consumed[p][r], 0);  // "consumed" initially
+    }
+  }
+  g->halo.assign(nranks, nullptr);
+  g->send_buf.assign(nranks, nullptr);
+  cudaDeviceSynchronize();
+  *out = g;
+  return RCG_OK;
+}
+
+extern "C" void rcg_loop_group_destroy(void* gp) {
+  LoopGroup* g = (LoopGroup*)gp;
+  if (!g) return;
+  cudaDeviceSynchronize();
+  for (int p = 0; p < 2; ++p)
+    for (int r = 0; r < g->nranks; ++r) {
+      if (g->slot[p][r]) cudaFree(g->slot[p][r]);
+      cudaEventDestroy(g->ready[p][r]);
+      cudaEventDestroy(g->consumed[p][r]);
+    }
+  delete g;
+}
+
+extern "C" int rcg_comm_init_loopback(rcg_ctx* ctx, void* group, int rank) {
+  LoopGroup* g = (LoopGroup*)group;
+  if (!ctx || !g || rank < 0 || rank >= g->nranks) return RCG_ERR_CONTRACT;
+  comm_free(ctx);
+  Comm* cm = new Comm();
+  cm->nranks = g->nranks;
+  cm->rank = rank;
+  cm->loop = g;
+  ctx->comm = cm;
+  return RCG_OK;
 }

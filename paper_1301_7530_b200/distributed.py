@@ -31,7 +31,8 @@ import numpy as np
 from . import _lib
 from .core import ContractViolation, SparseSpdMatrix
 
-__all__ = ["partition_rows", "HaloPlan", "build_local_system", "ShardedMatrix", "init_comm", "nccl_library"]
+__all__ = ["partition_rows", "HaloPlan", "build_local_system", "local_systems_all", "ShardedMatrix", "init_comm",
+           "init_loopback", "LoopbackGroup", "nccl_library"]
 
 
 def partition_rows(row_offsets, nranks, align=1):
@@ -68,7 +69,31 @@ class HaloPlan:
     ghost_global: np.ndarray  # global index of each ghost entry
 
 
-def build_local_system(ro, ci, va, bounds, rank, group=None):
+def _ghosts(ci, r0, r1, bounds, nranks):
+    ci = np.asarray(ci, dtype=np.int64)
+    owned = (ci >= r0) & (ci < r1)
+    ghosts = np.unique(ci[~owned])
+    owner = np.searchsorted(bounds, ghosts, side="right") - 1
+    return owned, ghosts, owner
+
+
+def local_systems_all(row_offsets, col_indices, values, bounds):
+    """Every rank's (ro, lci, va, plan) computed in one process (the needs
+    exchange done locally) — the same plans build_local_system produces over
+    torch.distributed; used by the single-GPU loopback validation."""
+    nranks = len(bounds) - 1
+    ro_g = np.asarray(row_offsets, dtype=np.int64)
+    parts, needs_all = [], []
+    for rank in range(nranks):
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        s, e = ro_g[r0], ro_g[r1]
+        _, ghosts, owner = _ghosts(col_indices[s:e], r0, r1, bounds, nranks)
+        needs_all.append([ghosts[owner == q] for q in range(nranks)])
+        parts.append((ro_g[r0:r1 + 1], col_indices[s:e], values[s:e]))
+    return [build_local_system(*parts[r], bounds, r, gathered=needs_all) for r in range(nranks)]
+
+
+def build_local_system(ro, ci, va, bounds, rank, group=None, gathered=None):
     """This rank's local CSR (owned + ghost column numbering) and halo plan.
 
     ``ro/ci/va`` are the rows of THIS rank only (global column indices),
@@ -77,7 +102,6 @@ def build_local_system(ro, ci, va, bounds, rank, group=None):
     symmetric by construction: rank p sends to q exactly the entries q asked
     p for, in q's ghost order.
     """
-    import torch.distributed as dist
     nranks = len(bounds) - 1
     r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
     n_local = r1 - r0
@@ -96,11 +120,13 @@ def build_local_system(ro, ci, va, bounds, rank, group=None):
     lci[~owned] = n_local + np.searchsorted(ghosts, ci[~owned])
     # who needs what from whom
     needs = [ghosts[owner == q] for q in range(nranks)]
-    gathered = [None] * nranks
-    if nranks > 1:
-        dist.all_gather_object(gathered, needs, group=group)
-    else:
-        gathered = [needs]
+    if gathered is None:
+        import torch.distributed as dist
+        gathered = [None] * nranks
+        if nranks > 1:
+            dist.all_gather_object(gathered, needs, group=group)
+        else:
+            gathered = [needs]
     send_lists = [np.asarray(gathered[q][rank], dtype=np.int64) - r0 if q != rank else np.zeros(0, np.int64)
                   for q in range(nranks)]
     for q, lst in enumerate(send_lists):
@@ -172,4 +198,31 @@ def init_comm(group=None):
     dist.broadcast_object_list(obj, src=0, group=group)
     idb = (C.c_char * 128).from_buffer_copy(obj[0])
     ctx.check(ctx.lib.rcg_comm_init(ctx.h, pb, idb, world, rank), "nccl comm init")
+    return ctx
+
+
+class LoopbackGroup:
+    """Single-process loopback transport for validating the sharded path on
+    one GPU: ``nranks`` host threads, each with its own CUDA stream and rcg
+    context, act as ranks (include/rcg.h rcg_loop_group_create)."""
+
+    def __init__(self, nranks):
+        lib = _lib.load()
+        h = C.c_void_p()
+        rc = lib.rcg_loop_group_create(int(nranks), C.byref(h))
+        if rc != 0:
+            raise RuntimeError(f"rcg_loop_group_create failed ({rc})")
+        self.h, self.nranks, self.lib = h, int(nranks), lib
+
+    def close(self):
+        if self.h:
+            self.lib.rcg_loop_group_destroy(self.h)
+            self.h = None
+
+
+def init_loopback(group: LoopbackGroup, rank):
+    """Bind this thread's rcg context (current device and stream) to rank
+    ``rank`` of a loopback group."""
+    ctx = _lib.context()
+    ctx.check(ctx.lib.rcg_comm_init_loopback(ctx.h, group.h, int(rank)), "loopback init")
     return ctx
