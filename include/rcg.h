@@ -283,6 +283,9 @@ int rcg_ritz_vectors(rcg_ctx* ctx, const double* alphas, const double* betas,
 /* column 2-norms of X (n x k) into norms[k] */
 int rcg_column_norms(rcg_ctx* ctx, int64_t n, int64_t k, const double* X, int64_t ldx,
                      double* norms);
+/* sharded: 2-norms of the global columns (local sums of squares allreduced) */
+int rcg_column_norms_sharded(rcg_ctx* ctx, int64_t n_local, int64_t k, const double* X, int64_t ldx,
+                             double* norms);
 /* Y[:, i] = X[:, i] / s[i] */
 int rcg_scale_columns(rcg_ctx* ctx, int64_t n, int64_t k, const double* X, int64_t ldx,
                       const double* s, double* Y, int64_t ldy);

@@ -116,6 +116,7 @@ SIGNATURES = {
     "rcg_ritz_select": (C.c_int, [_vp, _vp, _vp, _i64, _d, _vp, _vp, _vp, _vp, _vp]),
     "rcg_ritz_vectors": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _i64, _i32, _vp, _i64]),
     "rcg_column_norms": (C.c_int, [_vp, _i64, _i64, _vp, _i64, _vp]),
+    "rcg_column_norms_sharded": (C.c_int, [_vp, _i64, _i64, _vp, _i64, _vp]),
     "rcg_scale_columns": (C.c_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _i64]),
 }
 EXPORTS = tuple(SIGNATURES)

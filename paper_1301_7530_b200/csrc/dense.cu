@@ -9,6 +9,7 @@
 // would not change the bound).  Every reduction is fixed-order.
 #include "rcg_internal.cuh"
 #include "dense.cuh"
+#include "comm.cuh"
 
 #include <cmath>
 #include <vector>
@@ -297,13 +298,18 @@ int cholesky(Ctx* c, const double* G, int64_t n, double pivot_rtol, double* L, d
 // column norms / scaling (update_basis_trks, recycle.py:127-140)
 
 __global__ void __launch_bounds__(256)
-colnorm_kernel(int64_t n, const double* __restrict__ X, int64_t ldx, double* norms) {
+colnorm_kernel(int64_t n, const double* __restrict__ X, int64_t ldx, double* norms, int squared) {
   __shared__ double sm[8];
   const double* x = X + (int64_t)blockIdx.x * ldx;
   double s = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += x[i] * x[i];
   s = block_sum<256>(s, sm);
-  if (threadIdx.x == 0) norms[blockIdx.x] = sqrt(s);
+  if (threadIdx.x == 0) norms[blockIdx.x] = squared ? s : sqrt(s);
+}
+
+__global__ void sqrt_kernel(int64_t k, double* v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = sqrt(v[i]);
 }
 
 __global__ void scalecol_kernel(int64_t n, int64_t k, const double* __restrict__ X, int64_t ldx,
@@ -344,7 +350,20 @@ extern "C" int rcg_column_norms(rcg_ctx* ctx, int64_t n, int64_t k, const double
                                 double* norms) {
   if (!ctx) return RCG_ERR_CONTRACT;
   if (k == 0) return RCG_OK;
-  colnorm_kernel<<<(unsigned)k, 256, 0, ctx->stream>>>(n, X, ldx, norms);
+  colnorm_kernel<<<(unsigned)k, 256, 0, ctx->stream>>>(n, X, ldx, norms, 0);
+  RCG_LAUNCH_CHECK(ctx);
+  return RCG_OK;
+}
+
+extern "C" int rcg_column_norms_sharded(rcg_ctx* ctx, int64_t n, int64_t k, const double* X, int64_t ldx,
+                                        double* norms) {
+  if (!ctx) return RCG_ERR_CONTRACT;
+  if (k == 0) return RCG_OK;
+  colnorm_kernel<<<(unsigned)k, 256, 0, ctx->stream>>>(n, X, ldx, norms, 1);   // local sums of squares
+  RCG_LAUNCH_CHECK(ctx);
+  int rc = allreduce_sum(ctx, norms, (size_t)k);                                 // over the row slabs
+  if (rc) return rc;
+  sqrt_kernel<<<(unsigned)std::min<int64_t>(ceil_div(k, 256), 64), 256, 0, ctx->stream>>>(k, norms);
   RCG_LAUNCH_CHECK(ctx);
   return RCG_OK;
 }

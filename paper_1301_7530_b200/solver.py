@@ -514,6 +514,7 @@ def apcg_solve(A: SparseSpdMatrix, M: Preconditioner, D: DeflationOperator, b, c
         trace.w_history = _history(owner, view.W, ld, m, A.n, cap_cols=m + 1)
         trace.r_history = _history(owner, view.R, ld, m, A.n, cap_cols=m + 1)
     trace.projection_seconds = 0.0
+    trace.sharded = hasattr(A, "plan")
     if rc == _lib.RCG_ERR_NUMERICAL:
         ctx.check(rc, "apcg_solve")
     ctx.check(rc, "apcg_solve")

@@ -91,3 +91,28 @@ def test_sharded_srks_sequence_matches_unsharded():
     got, want = res[0][0], ref.iterations()
     assert all(abs(g - w) <= max(1, 0.02 * w) for g, w in zip(got, want)), (got, want)
     assert all(abs(a - b) <= 2 for a, b in zip(res[0][1], ref.n_c_history()))
+
+
+def test_sharded_trks_sequence_matches_unsharded():
+    seq = list(problems.generate_diffusion_sequence(problems.benchmark_spec(seed=0), 3))
+    A0 = seq[0][0]
+    cfg = rcg.SolveConfig(tol=1e-3, max_iters=3000)
+    strat = rcg.RecycleStrategy("trks")
+    ref = rcg.run_sequence(iter(seq), rcg.Preconditioner.jacobi, strat, cfg)
+    parts = []
+    for A, b in seq:
+        bounds = Dm.partition_rows(A.row_offsets, 2)
+        parts.append((bounds, Dm.local_systems_all(A.row_offsets, A.col_indices, A.values, bounds), b))
+
+    def fn(r):
+        systems = []
+        for bounds, loc, b in parts:
+            ro, lci, va, plan = loc[r]
+            r0, r1 = int(bounds[r]), int(bounds[r + 1])
+            systems.append((Dm.ShardedMatrix(ro, lci, va, plan, A0.n), b[r0:r1].copy()))
+        rep = rcg.run_sequence(iter(systems), rcg.Preconditioner.jacobi, strat, cfg)
+        return rep.iterations(), rep.n_c_history()
+    res = _run_ranks(2, fn)
+    assert res[0] == res[1]
+    assert all(abs(g - w) <= max(1, 0.02 * w) for g, w in zip(res[0][0], ref.iterations())), (res[0], ref.iterations())
+    assert res[0][1] == ref.n_c_history()
