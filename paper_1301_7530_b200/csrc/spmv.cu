@@ -18,6 +18,13 @@
 #include <algorithm>
 #include <cstdlib>
 
+#ifndef RCG_SPMV_MINB
+#define RCG_SPMV_MINB 4
+#endif
+#ifndef RCG_SPMV_U8
+#define RCG_SPMV_U8 12
+#endif
+
 namespace rcg {
 
 template <typename RO, int V, int MODE>
@@ -33,7 +40,7 @@ __device__ __forceinline__ void spmv_body(int64_t n, const RO* __restrict__ ro, 
   const double* __restrict__ x = xs.at(j);
   double* __restrict__ y = ys.at(j);
   constexpr int RPW = 32 / V;                 // rows per warp step
-  constexpr int U = V == 1 ? 8 : 12;          // fast path: <= U*V entries per row
+  constexpr int U = V == 1 ? 8 : RCG_SPMV_U8;  // fast path: <= U*V entries per row
   const int lane = threadIdx.x & 31;
   const int sub = lane % V;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -228,7 +235,7 @@ __device__ __forceinline__ void bsr3_body(int64_t nbr, const int32_t* __restrict
 }
 
 template <typename RO, int V, int MODE>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, RCG_SPMV_MINB)
 spmv_kernel(int64_t n, const RO* __restrict__ ro, const int32_t* __restrict__ ci,
             const double* __restrict__ va, ColSel xs, ColSel ys, const double* __restrict__ b,
             const SolveState* st, double* part, unsigned int* counter, double* out) {
@@ -247,7 +254,7 @@ bsr3_kernel(int64_t nbr, const int32_t* __restrict__ bro, const int32_t* __restr
 // device-resident SpmvArgs, so one captured CUDA graph serves every
 // iteration, batch and solve of a sequence (see pcg.cu).
 template <typename RO, int V>
-__global__ void __launch_bounds__(kThreads) spmv_kernel_ind(const SpmvArgs* __restrict__ sa) {
+__global__ void __launch_bounds__(kThreads, RCG_SPMV_MINB) spmv_kernel_ind(const SpmvArgs* __restrict__ sa) {
   spmv_body<RO, V, 1>(sa->n, (const RO*)sa->ro, sa->ci, sa->va, sa->xs, sa->ys, nullptr, sa->st, sa->part,
                       sa->counter, sa->out);
 }
