@@ -219,7 +219,6 @@ update_kernel(const IterArgs* __restrict__ ap, int init) {
       if (a.waw_diag) a.waw_diag[j] = wAw;
     }
   }
-  extern __shared__ double ytile[];
   __shared__ double sm[kWarps];
   const int64_t r0 = (int64_t)blockIdx.x * a.rows_per_block_upd;
   const int64_t r1 = min(a.n, r0 + a.rows_per_block_upd);
@@ -236,18 +235,86 @@ update_kernel(const IterArgs* __restrict__ ap, int init) {
       a.r[i] = ri;
     }
     rr += ri * ri;
-    if (a.n_c) ytile[i - r0] = a.inv_diag ? __dmul_rn(a.inv_diag[i], ri) : ri;
   }
+  // ||r||^2 partial in column 0 of the [tile][1 + n_c] partial rows; the
+  // AC^T y columns come from actr_kernel (same tiles)
   const int64_t K = 1 + a.n_c;
   const double rrb = block_sum<kThreads>(rr, sm);
   if (threadIdx.x == 0) a.part_upd[(size_t)blockIdx.x * K] = rrb;
-  if (a.n_c) {
-    __syncthreads();
-    __shared__ double red[kWarps * 8];
-    gemv_t_tile<8, 1>(a.AC + r0, a.ldac, a.n_c, r1 - r0, ytile, nullptr, a.part_upd + (size_t)blockIdx.x * K + 1,
-                      red);
+  if (arrive_last(a.counters + 1)) reduce_partials_strided<kThreads>(a.part_upd, gridDim.x, (int)K, 1, a.sums + 1);
+}
+
+// AC^T (M^{-1} r) for the projector (solver.py:84-91): grid (row tiles, groups
+// of 8 columns).  The 8 warps split the tile's rows; lanes read 2 rows per
+// column with one 128-bit load; y = inv_diag * r is recomputed exactly as in
+// the reference (one rounding).  Partials go to columns 1..n_c of the
+// [tile][1 + n_c] rows; the last CTA reduces them in a fixed order.
+__global__ void __launch_bounds__(kThreads)
+actr_kernel(const IterArgs* __restrict__ ap) {
+  const IterArgs& a = *ap;
+  if (a.st->done) return;
+  constexpr int CG = 8;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t tile = blockIdx.x, k0 = (int64_t)blockIdx.y * CG;
+  const int kc = (int)min((int64_t)CG, a.n_c - k0);
+  const int64_t r0 = tile * a.rows_per_block_upd;
+  const int64_t len = min(a.n, r0 + a.rows_per_block_upd) - r0;
+  const int64_t pairs = len >> 1, per = (pairs + kWarps - 1) / kWarps;
+  const int64_t pb = wid * per, pe = min(pairs, pb + per);
+  const double* __restrict__ cols = a.AC + k0 * a.ldac + r0;
+  const double* __restrict__ rr = a.r + r0;
+  const double* __restrict__ inv = a.inv_diag ? a.inv_diag + r0 : nullptr;
+  double acc[CG];
+#pragma unroll
+  for (int c = 0; c < CG; ++c) acc[c] = 0.0;
+#pragma unroll 2
+  for (int64_t pi = pb + lane; pi < pe; pi += 32) {
+    double2 y = *reinterpret_cast<const double2*>(rr + 2 * pi);
+    if (inv) {
+      const double2 d = *reinterpret_cast<const double2*>(inv + 2 * pi);
+      y.x = __dmul_rn(d.x, y.x);
+      y.y = __dmul_rn(d.y, y.y);
+    }
+#pragma unroll
+    for (int c = 0; c < CG; ++c)
+      if (c < kc) {
+        const double2 v = __ldcs(reinterpret_cast<const double2*>(cols + c * a.ldac) + pi);
+        acc[c] += v.x * y.x + v.y * y.y;
+      }
   }
-  if (arrive_last(a.counters + 1)) reduce_partials<kThreads>(a.part_upd, gridDim.x, (int)K, a.sums + 1);
+  if ((len & 1) && wid == kWarps - 1 && lane == 0) {
+    const int64_t i = len - 1;
+    const double y = inv ? __dmul_rn(inv[i], rr[i]) : rr[i];
+#pragma unroll
+    for (int c = 0; c < CG; ++c)
+      if (c < kc) acc[c] += cols[c * a.ldac + i] * y;
+  }
+  __shared__ double red[kWarps][CG];
+#pragma unroll
+  for (int c = 0; c < CG; ++c) {
+    const double s = warp_sum(acc[c]);
+    if (lane == 0) red[wid][c] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < kc) {
+    double s = 0.0;
+    for (int q = 0; q < kWarps; ++q) s += red[q][threadIdx.x];   // warp order: fixed
+    a.part_upd[(size_t)tile * (1 + a.n_c) + 1 + k0 + threadIdx.x] = s;
+  }
+  // last CTA of the 2-D grid reduces the AC^T y columns over the tiles
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int prev = atomicAdd(a.counters + 3, 1u);
+    last = (prev == gridDim.x * gridDim.y - 1);
+    if (last) a.counters[3] = 0u;
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    reduce_partials_strided<kThreads>(a.part_upd + 1, (int)gridDim.x, (int)(1 + a.n_c), (int)a.n_c, a.sums + 2);
+  }
 }
 
 // coarse solve s = G^{-1} (AC^T y) for n_c > NC_INLINE: one warp per row of
@@ -793,7 +860,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   };
   const int R = reorth ? rows_per_block_for(c, n) : big_tile(rows_per_block_for(c, n));
   const int nb = (int)std::max<int64_t>(1, ceil_div(n, R));
-  static const int upd_tiles = env_int("RCG_UPD_TILES_PER_SM", 8);
+  static const int upd_tiles = env_int("RCG_UPD_TILES_PER_SM", 4);
   const int Ru = n_c ? rows_per_block_for(c, n, upd_tiles) : big_tile(rows_per_block_for(c, n, upd_tiles));
   const int nbu = (int)std::max<int64_t>(1, ceil_div(n, Ru));
   const int nbs = spmv_partials(c, A);
@@ -1031,8 +1098,12 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   };
 
   // ---- z0, rz0, w0 (solver.py:221-231) ----
-  update_kernel<<<nbu_l, kThreads, smem_upd, c->stream>>>(dargs, 1);
+  update_kernel<<<nbu_l, kThreads, 0, c->stream>>>(dargs, 1);
   RCG_LAUNCH_CHECK(c);
+  if (n_c) {
+    actr_kernel<<<dim3(nbu, (unsigned)ceil_div(n_c, 8)), kThreads, 0, c->stream>>>(dargs);
+    RCG_LAUNCH_CHECK(c);
+  }
   if ((rc = allreduce_h(H, c, gSum.ptr + 1, (size_t)(1 + n_c)))) return fail(rc);
   if ((rc = launch_coarse(1))) return fail(rc);
   pre<<<nb_l, kThreads, smem_pre, c->stream>>>(dargs, 1);
@@ -1075,8 +1146,12 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
       if (direct) prof_end(c);
       if ((rc2 = allreduce_h(H, c, gSum.ptr, 1))) return rc2;
       if (direct) prof_begin(c, RCG_K_UPDATE, 8.0 * nd * (6 + jac + n_c + (store ? 1 : 0)));
-      update_kernel<<<nbu_l, kThreads, smem_upd, c->stream>>>(dargs, 0);
+      update_kernel<<<nbu_l, kThreads, 0, c->stream>>>(dargs, 0);
       RCG_LAUNCH_CHECK(c);
+      if (n_c) {
+        actr_kernel<<<dim3(nbu, (unsigned)ceil_div(n_c, 8)), kThreads, 0, c->stream>>>(dargs);
+        RCG_LAUNCH_CHECK(c);
+      }
       if (direct) prof_end(c);
       if ((rc2 = allreduce_h(H, c, gSum.ptr + 1, (size_t)(1 + n_c)))) return rc2;
       if (n_c > NC_INLINE) {
@@ -1138,7 +1213,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
       char key[256];
       snprintf(key, sizeof(key), "%p|%lld|%d|%d|%d|%d|%zu|%zu|%d|%d|%lld|%d|%d", (void*)pre, (long long)n,
                spmv_width(A), nbs, nb, nbu, smem_upd, smem_pre, reorth ? 1 : 0, n_c > NC_INLINE ? 1 : 0,
-               (long long)B, A->block, A->row_offsets_64);
+               (long long)B, A->block, A->row_offsets_64 + 2 * (int)ceil_div(n_c, 8));
       cudaGraphExec_t exec = nullptr;
       auto gi = c->graphs.find(key);
       if (gi != c->graphs.end()) {

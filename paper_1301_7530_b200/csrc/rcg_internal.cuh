@@ -163,6 +163,18 @@ __device__ void reduce_partials(const double* part, int nb, int K, double* out) 
   }
 }
 
+// as reduce_partials, for `count` values at stride `stride` in each partial row
+template <int NT>
+__device__ void reduce_partials_strided(const double* part, int nb, int stride, int count, double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int k = wid; k < count; k += NT / 32) {
+    double s = 0.0;
+    for (int b = lane; b < nb; b += 32) s += __ldcg(part + (size_t)b * stride + k);
+    s = warp_sum(s);
+    if (lane == 0) out[k] = s;
+  }
+}
+
 __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ __forceinline__ int64_t pad_ld(int64_t n) { return ceil_div(n, 32) * 32; }
 
