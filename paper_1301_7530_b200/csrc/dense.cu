@@ -99,54 +99,68 @@ int gemm_tn(Ctx* c, int64_t n, int64_t a, int64_t b, const double* X, int64_t ld
 }
 
 // ---------------------------------------------------------------------------
-// Y = X Q  (n x m) (m x s), tile 64 rows x 32 cols, k-slab 32
+// Y = X Q  (n x m) (m x s), tile 64 rows x 64 cols (4x4 per thread), k-slab
+// 32: for s <= 64 selected Ritz vectors the history X is streamed once.
 
 __global__ void __launch_bounds__(256)
 gemm_nn_kernel(int64_t n, int64_t m, int64_t s, const double* __restrict__ X, int64_t ldx,
                const double* __restrict__ Q, int64_t ldq, double* __restrict__ Y, int64_t ldy) {
-  __shared__ double Xs[32][64];
-  __shared__ double Qs[32][33];
+  __shared__ double Xs[32][64 + 1];
+  __shared__ double Qs[32][64 + 1];
   const int t = threadIdx.x;
-  const int r = t & 63;
-  const int c0 = (t >> 6) * 8;
+  const int tr = t & 15, tc = t >> 4;          // 16 x 16 threads
   const int64_t row0 = (int64_t)blockIdx.x * 64;
-  const int64_t col0 = (int64_t)blockIdx.y * 32;
-  double acc[8];
+  const int64_t col0 = (int64_t)blockIdx.y * 64;
+  double acc[4][4];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[i][q] = 0.0;
   for (int64_t k0 = 0; k0 < m; k0 += 32) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int kk = (t >> 6) + 4 * q;  // 0..31
+    for (int q = 0; q < 8; ++q) {             // 32 x 64 slab of X, rows contiguous
+      const int e = t + 256 * q;
+      const int kk = e >> 6, r = e & 63;
       const int64_t row = row0 + r;
-      Xs[kk][r] = (row < n && k0 + kk < m) ? X[(k0 + kk) * ldx + row] : 0.0;
+      Xs[kk][r] = (row < n && k0 + kk < m) ? __ldcs(X + (k0 + kk) * ldx + row) : 0.0;
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int kk = t & 31, cc = (t >> 5) + 8 * q;
+    for (int q = 0; q < 8; ++q) {             // 32 x 64 slab of Q
+      const int e = t + 256 * q;
+      const int kk = e & 31, cc = e >> 5;
       Qs[kk][cc] = (k0 + kk < m && col0 + cc < s) ? Q[(col0 + cc) * ldq + k0 + kk] : 0.0;
     }
     __syncthreads();
 #pragma unroll 8
     for (int kk = 0; kk < 32; ++kk) {
-      const double xv = Xs[kk][r];
+      double xv[4], qv[4];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q] += xv * Qs[kk][c0 + q];
+      for (int i = 0; i < 4; ++i) xv[i] = Xs[kk][tr + 16 * i];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) qv[q] = Qs[kk][tc + 16 * q];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[i][q] += xv[i] * qv[q];
     }
     __syncthreads();
   }
-  const int64_t row = row0 + r;
-  if (row < n) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (col0 + c0 + q < s) Y[(col0 + c0 + q) * ldy + row] = acc[q];
+  for (int i = 0; i < 4; ++i) {
+    const int64_t row = row0 + tr + 16 * i;
+    if (row >= n) continue;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t col = col0 + tc + 16 * q;
+      if (col < s) Y[col * ldy + row] = acc[i][q];
+    }
   }
 }
 
 int gemm_nn(Ctx* c, int64_t n, int64_t m, int64_t s, const double* X, int64_t ldx, const double* Q,
             int64_t ldq, double* Y, int64_t ldy) {
   if (n == 0 || s == 0) return RCG_OK;
-  dim3 grid((unsigned)ceil_div(n, 64), (unsigned)ceil_div(s, 32));
+  dim3 grid((unsigned)ceil_div(n, 64), (unsigned)ceil_div(s, 64));
   gemm_nn_kernel<<<grid, 256, 0, c->stream>>>(n, m, s, X, ldx, Q, ldq, Y, ldy);
   RCG_LAUNCH_CHECK(c);
   return RCG_OK;

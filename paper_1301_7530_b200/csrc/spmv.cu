@@ -313,6 +313,76 @@ __global__ void block3_build_kernel(int64_t nbr, const RO* __restrict__ ro, cons
   }
 }
 
+int spmv_grid(Ctx* c, const rcg_csr* A, int V);
+
+// Y[:, c] = A X[:, c] for CB columns at once: V lanes per row, each matrix
+// entry loaded once and applied to the CB columns (the CB-column slab of X is
+// L2-resident); used by build_deflation (AC = A C, solver.py:113).
+template <typename RO, int V, int CB>
+__global__ void __launch_bounds__(kThreads)
+spmm_kernel(int64_t n, const RO* __restrict__ ro, const int32_t* __restrict__ ci, const double* __restrict__ va,
+            const double* __restrict__ X, int64_t ldx, int kc, double* __restrict__ Y, int64_t ldy) {
+  constexpr int RPW = 32 / V;
+  const int lane = threadIdx.x & 31, sub = lane % V;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r0 = warp * RPW; r0 < n; r0 += nwarps * RPW) {
+    const int64_t row = r0 + lane / V;
+    double acc[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) acc[c] = 0.0;
+    if (row < n) {
+      const int64_t rs = ro_at(ro, row), re = ro_at(ro, row + 1);
+      for (int64_t k = rs + sub; k < re; k += V) {
+        const double v = __ldg(va + k);
+        const int64_t col = __ldg(ci + k);
+#pragma unroll
+        for (int c = 0; c < CB; ++c)
+          if (c < kc) acc[c] += v * __ldg(X + c * ldx + col);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < CB; ++c) {
+#pragma unroll
+      for (int o = V / 2; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+    }
+    if (row < n && sub == 0) {
+#pragma unroll
+      for (int c = 0; c < CB; ++c)
+        if (c < kc) Y[c * ldy + row] = acc[c];
+    }
+  }
+}
+
+int launch_spmm(Ctx* c, const rcg_csr* A, const double* X, int64_t ldx, int64_t k, double* Y, int64_t ldy) {
+  constexpr int CB = 8;
+  const int64_t avg = A->n ? A->nnz / A->n : 0;
+  for (int64_t c0 = 0; c0 < k; c0 += CB) {
+    const int kc = (int)std::min<int64_t>(CB, k - c0);
+    const double* Xc = X + c0 * ldx;
+    double* Yc = Y + c0 * ldy;
+    if (avg > 10) {
+      const int grid = spmv_grid(c, A, 8);
+      if (A->row_offsets_64)
+        spmm_kernel<int64_t, 8, CB><<<grid, kThreads, 0, c->stream>>>(A->n, (const int64_t*)A->row_offsets,
+                                                                     A->col_indices, A->values, Xc, ldx, kc, Yc, ldy);
+      else
+        spmm_kernel<int32_t, 8, CB><<<grid, kThreads, 0, c->stream>>>(A->n, (const int32_t*)A->row_offsets,
+                                                                     A->col_indices, A->values, Xc, ldx, kc, Yc, ldy);
+    } else {
+      const int grid = spmv_grid(c, A, 1);
+      if (A->row_offsets_64)
+        spmm_kernel<int64_t, 1, CB><<<grid, kThreads, 0, c->stream>>>(A->n, (const int64_t*)A->row_offsets,
+                                                                     A->col_indices, A->values, Xc, ldx, kc, Yc, ldy);
+      else
+        spmm_kernel<int32_t, 1, CB><<<grid, kThreads, 0, c->stream>>>(A->n, (const int32_t*)A->row_offsets,
+                                                                     A->col_indices, A->values, Xc, ldx, kc, Yc, ldy);
+    }
+    RCG_LAUNCH_CHECK(c);
+  }
+  return RCG_OK;
+}
+
 int spmv_width(const rcg_csr* A) {
   static int forced = -1;
   if (forced < 0) {
@@ -497,12 +567,7 @@ extern "C" int rcg_spmv(rcg_ctx* ctx, const rcg_csr* A, const double* x, double*
 extern "C" int rcg_spmm(rcg_ctx* ctx, const rcg_csr* A, const double* X, int64_t ldx, int64_t k,
                         double* Y, int64_t ldy) {
   if (!ctx || !A || ldx < A->n || ldy < A->n) return ctx ? set_error(ctx, RCG_ERR_CONTRACT, "rcg_spmm: bad ld") : RCG_ERR_CONTRACT;
-  for (int64_t c = 0; c < k; ++c) {
-    int rc = launch_spmv(ctx, A, 0, colsel((double*)X + c * ldx), colsel(Y + c * ldy), nullptr, nullptr,
-                         nullptr, nullptr, nullptr);
-    if (rc) return rc;
-  }
-  return RCG_OK;
+  return launch_spmm(ctx, A, X, ldx, k, Y, ldy);
 }
 
 extern "C" int rcg_csr_diagonal(rcg_ctx* ctx, const rcg_csr* A, double* diag, double* inv_diag) {
