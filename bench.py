@@ -243,6 +243,7 @@ def run_ours(args):
         D.init_comm()
         A = D.ShardedMatrix(ro_l, lci, va, plan, A_global.n)
         bs = [b[r0:r1].copy() for b in bs]
+        shard_host = (ro_l, lci, va, plan)
     bs_dev = [torch.from_numpy(b).to("cuda") for b in bs]
     A.device_csr()
 
@@ -313,15 +314,20 @@ def run_ours(args):
 
     # e2e: public API with host arrays; CSR + RHS uploads and x downloads timed
     e2e = None
-    if not args.no_e2e and not sharded:
+    if not args.no_e2e:
         ro, ci, va = A.row_offsets, A.col_indices, A.values
+        # per rank: its CSR slab (+ halo plan) and RHS slices cross PCIe every step
         h2d = 4 * (A.n + 1) + 4 * A.nnz + 8 * A.nnz + 8 * A.n * len(bs)
         e2e_iters, d2h = 0, 0
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            Ah = rcg.SparseSpdMatrix(A.n, ro, ci, va, validate=False)  # fresh: uploaded inside the region
+            if sharded:   # fresh slab object: CSR + halo lists uploaded inside the region
+                from paper_1301_7530_b200 import distributed as D
+                Ah = D.ShardedMatrix(*shard_host, A_global.n)
+            else:         # fresh: uploaded inside the region
+                Ah = rcg.SparseSpdMatrix(A.n, ro, ci, va, validate=False)
             xs = []
             systems = ((Ah, b) for b in bs)
             rep2 = _e2e_sequence(rcg, systems, strat, cfg, xs)
@@ -330,7 +336,12 @@ def run_ours(args):
         torch.cuda.synchronize()
         barrier()
         sec2 = max_over_ranks(time.perf_counter() - t0)
-        e2e = {"value": world * e2e_iters / sec2, "unit": UNIT, "h2d_bytes_per_step": h2d,
+        if sharded:   # bytes summed over ranks; one joint sequence
+            t = torch.tensor([float(h2d), float(d2h)], dtype=torch.float64, device="cuda")
+            import torch.distributed as dist
+            dist.all_reduce(t)
+            h2d, d2h = int(t[0].item()), int(t[1].item())
+        e2e = {"value": (e2e_iters if sharded else world * e2e_iters) / sec2, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h // max(args.steps, 1), "sequence_seconds": sec2 / args.steps}
 
     cpu = None
@@ -362,10 +373,9 @@ def _e2e_sequence(rcg, systems, strat, cfg, xs):
     """run_sequence with host RHS; solutions come back as host arrays."""
     rep = rcg.SequenceReport()
     state = None
-    import time as _t
     for k, (A, b) in enumerate(systems):
         if state is None:
-            state = rcg.AugmentationState.from_initial(A.n)
+            state = rcg.AugmentationState.from_initial(A.n, None, getattr(A, "n_ext", None))
         ncb = state.n_c
         D = rcg.guarded_deflation(A, state, rep.events)
         x, tr = rcg.apcg_solve(A, rcg.Preconditioner.jacobi(A), D, b, cfg)   # b host -> x host
