@@ -209,6 +209,25 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def box_copy_gbps():
+    import torch
+    try:
+        a = torch.empty(1 << 29, dtype=torch.bfloat16, device="cuda")
+        b = torch.empty_like(a)
+        best = 0.0
+        for _ in range(6):
+            e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            e0.record()
+            b.copy_(a)
+            e1.record()
+            torch.cuda.synchronize()
+            best = max(best, 2 * a.numel() * 2 / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+        del a, b
+        return best
+    except Exception:
+        return None
+
+
 def ncu_traffic():
     f = REPO / "profiles" / "ncu_traffic.json"
     try:
@@ -299,12 +318,17 @@ def run_ours(args):
     dom = max(stats, key=lambda k: stats[k]["seconds"])
     tot_k = sum(s["seconds"] for s in stats.values())
     peak, peak_src = peaks()
+    box_copy = box_copy_gbps()
     d = stats[dom]
     achieved = d["bytes"] / d["seconds"] / 1e9 if d["seconds"] > 0 else 0.0
     traffic = ncu_traffic().get(dom)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                 "share_of_kernel_time": d["seconds"] / tot_k if tot_k else None,
+                # context only (frac uses the driver-measured peak): this box's own copy
+                # bandwidth, measured like MEASURED_PEAKS.json (1 GiB copy_, best of 5)
+                "box_copy_GBps": box_copy,
+                "frac_of_box_copy": achieved / box_copy if box_copy else None,
                 "bytes_per_launch": d["bytes"] / max(d["launches"], 1),
                 "avg_launch_us": 1e6 * d["seconds"] / max(d["launches"], 1),
                 "all_kernels": {k: {"launches": s["launches"], "seconds": round(s["seconds"], 6),

@@ -40,7 +40,8 @@ __device__ __forceinline__ void spmv_body(int64_t n, const RO* __restrict__ ro, 
   const double* __restrict__ x = xs.at(j);
   double* __restrict__ y = ys.at(j);
   constexpr int RPW = 32 / V;                 // rows per warp step
-  constexpr int U = V == 1 ? 8 : RCG_SPMV_U8;  // fast path: <= U*V entries per row
+  // fast path: <= U*V entries per row, all loads issued before any gather
+  constexpr int U = V == 1 ? 8 : (V == 2 ? 8 : (V == 4 ? 12 : (V == 8 ? RCG_SPMV_U8 : (V == 16 ? 6 : 3))));
   const int lane = threadIdx.x & 31;
   const int sub = lane % V;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
