@@ -269,7 +269,8 @@ def run_ours(args):
     def step():
         rep = rcg.run_sequence(((A, b) for b in bs_dev), rcg.Preconditioner.jacobi, strat, cfg)
         if rep.aborted or not all(r.converged for r in rep.records):
-            raise RuntimeError(f"sequence did not converge: {rep.events}")
+            raise RuntimeError(f"sequence did not converge: {rep.events} "
+                               f"iterations={[r.iterations for r in rep.records]}")
         return rep
 
     def barrier():

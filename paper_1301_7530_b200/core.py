@@ -11,6 +11,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import os as _os
+
 import numpy as np
 
 from .core_errors import ContractViolation, NumericalFailure, RankDeficient
@@ -118,7 +120,7 @@ class SparseSpdMatrix:
     col_indices: np.ndarray
     values: np.ndarray
     validate: bool = field(default=True, repr=False, compare=False)
-    use_block3: bool = field(default=False, repr=False, compare=False)
+    use_block3: bool = field(default=True, repr=False, compare=False)
 
     def __post_init__(self):
         ro = np.asarray(self.row_offsets, dtype=np.int64)
@@ -204,7 +206,7 @@ class SparseSpdMatrix:
             ci = torch.from_numpy(np.ascontiguousarray(self.col_indices, dtype=np.int32)).to("cuda")
             va = torch.from_numpy(self.values).to("cuda")
             h = _DevCsr(ro, ci, va, self.n, self.nnz, ro64)
-            if self.use_block3 and self.n % 3 == 0 and self.nnz % 9 == 0 and self.nnz >= 9 * self.n // 3 * 2:
+            if self.use_block3 and _os.environ.get("RCG_BSR", "1") != "0" and self.n % 3 == 0 and self.nnz % 9 == 0 and self.nnz >= 9 * self.n // 3 * 2:
                 h.add_block3(_lib.context())
             self._dev[dev] = h
         return h

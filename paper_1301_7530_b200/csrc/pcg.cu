@@ -889,7 +889,10 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   if ((rc = alloc(sizeof(double) * 5 * nh, (void**)&hist))) return fail(rc);
   if ((rc = alloc(sizeof(double) * ld, (void**)&r))) return fail(rc);
   if ((rc = alloc(sizeof(double) * nbu * (1 + n_c), (void**)&part_upd))) return fail(rc);
-  if ((rc = alloc(sizeof(double) * (nb + 2 * nbs + 64), (void**)&part_z))) return fail(rc);
+  // part_spmv holds 2 partials per CTA of the SpMV (mode 2) AND of copy_norms
+  // (n_c = 0 initial residual), whose grids differ (BSR3 SpMV: 4 CTAs/SM)
+  const int nps = std::max(nbs, elementwise_grid(c, n));
+  if ((rc = alloc(sizeof(double) * (nb + 2 * nps + 64), (void**)&part_z))) return fail(rc);
   part_spmv = part_z + nb + 32;
   if ((rc = alloc(sizeof(double) * (n_c + 1), (void**)&s_ext))) return fail(rc);
   const size_t n_counters = 16 + (size_t)wu_grid;
@@ -1270,6 +1273,16 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   c->m_hint[n] = T->view.iterations;
   finish_view();
   *trace_out = T;
+  if (hst->failure && getenv("RCG_DEBUG_FAIL")) {
+    const int64_t jj = hst->j;
+    std::vector<double> al(std::max<int64_t>(jj + 1, 1)), ww(std::max<int64_t>(jj + 1, 1));
+    cudaMemcpy(al.data(), alphas, sizeof(double) * al.size(), cudaMemcpyDeviceToHost);
+    cudaMemcpy(ww.data(), wawd, sizeof(double) * ww.size(), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[rcg debug] failure %d at j=%lld n=%lld n_c=%lld block=%d\n", hst->failure, (long long)jj,
+            (long long)n, (long long)n_c, A->block);
+    for (int64_t k = std::max<int64_t>(0, jj - 4); k <= jj; ++k)
+      fprintf(stderr, "  k=%lld alpha=%.17g waw=%.17g\n", (long long)k, al[k], ww[k]);
+  }
   if (hst->failure) {
     return set_error(c, RCG_ERR_NUMERICAL, "%s",
                      hst->failure == RCG_FAIL_RZ ? "(r, z) <= 0: preconditioner or operator not SPD"

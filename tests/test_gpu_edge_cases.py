@@ -45,7 +45,11 @@ def test_max_iters_one_and_trailing_beta(rng):
 
 
 def test_reorth_off_and_no_capture_match_oracle(rng):
-    A = _spd(60, rng, 1e3)
+    # without reorthogonalization the iteration count of this n=60, cond 1e3
+    # system depends on rounding (> n iterations), so the SpMV must sum rows in
+    # the oracle's scalar-CSR order: disable the (dense => 3x3-block) BSR3 copy
+    A0 = _spd(60, rng, 1e3)
+    A = rcg.SparseSpdMatrix(A0.n, A0.row_offsets, A0.col_indices, A0.values, validate=False, use_block3=False)
     b = rng.standard_normal(60)
     C = rng.standard_normal((60, 5))
     cfg = rcg.SolveConfig(tol=1e-8, max_iters=500, reorthogonalize=False, trace_capture=False)
