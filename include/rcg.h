@@ -144,6 +144,9 @@ int rcg_ctx_set_stream(rcg_ctx* ctx, void* cuda_stream);
 const char* rcg_last_error(const rcg_ctx* ctx);
 int rcg_version(void);
 int rcg_num_kernel_launches(const rcg_ctx* ctx, int64_t* out_host); /* launches issued by ctx */
+/* Debug (RCG_POOL_GUARD=1 runs): re-verify every live pool buffer's canary zone and
+   return the number of write-past-the-end violations seen so far (0 when the guard is off). */
+int64_t rcg_debug_guard_violations(void);
 
 /* Live per-kernel-class timing of the solve loop: when enabled, every
  * iteration kernel is bracketed by CUDA events on the ctx stream and its

@@ -78,6 +78,7 @@ SIGNATURES = {
     "rcg_last_error": (C.c_char_p, [_vp]),
     "rcg_version": (C.c_int, []),
     "rcg_num_kernel_launches": (C.c_int, [_vp, c_int64_p]),
+    "rcg_debug_guard_violations": (C.c_int64, []),
     "rcg_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "rcg_ctx_kernel_stats": (C.c_int, [_vp, C.POINTER(RcgKernelStat), C.c_int]),
     "rcg_ctx_reset_stats": (C.c_int, [_vp]),

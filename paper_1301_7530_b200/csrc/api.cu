@@ -4,6 +4,10 @@
 #include "vmm.cuh"
 
 #include <cstdlib>
+#include <cstdio>
+#include <map>
+#include <mutex>
+#include <vector>
 #include <cstring>
 
 namespace rcg {
@@ -19,7 +23,19 @@ int set_error(Ctx* c, int code, const char* fmt, ...) {
   return code;
 }
 
+static bool pool_guard();
+static void guard_release(void* p);
+static void* guard_alloc(size_t bytes);
+
 int scratch(Ctx* c, size_t bytes, void** out) {
+  if (pool_guard()) {  // exact size + canary per call (see Pool::get)
+    if (c->scratch) guard_release(c->scratch);
+    c->scratch = guard_alloc(bytes);
+    c->scratch_bytes = bytes;
+    if (!c->scratch) return set_error(c, RCG_ERR_OOM, "scratch allocation of %zu bytes failed", bytes);
+    *out = c->scratch;
+    return RCG_OK;
+  }
   bytes = (bytes + 255) & ~(size_t)255;
   if (bytes > c->scratch_bytes) {
     if (c->scratch) cudaFreeAsync(c->scratch, c->stream);
@@ -46,7 +62,88 @@ void Pool::trim() {
   free_bytes = 0;
 }
 
+// RCG_POOL_EXACT=1: no pooling, exact-size cudaMalloc/cudaFree, so that
+// compute-sanitizer memcheck sees every out-of-bounds access (debug runs)
+static bool pool_exact() {
+  static const bool e = [] {
+    const char* v = getenv("RCG_POOL_EXACT");
+    return v && atoi(v) != 0;
+  }();
+  return e;
+}
+
+// RCG_POOL_GUARD=1: exact-size allocations followed by a canary zone that is
+// verified when the buffer is returned (and at context teardown): catches
+// kernels writing past the end of a pooled buffer (debug runs; slow)
+static bool pool_guard() {
+  static const bool e = [] {
+    const char* v = getenv("RCG_POOL_GUARD");
+    return v && atoi(v) != 0;
+  }();
+  return e;
+}
+static constexpr size_t kGuard = 64 << 10;
+static constexpr unsigned char kCanary = 0xA5;
+static std::mutex g_guard_mu;
+static std::map<void*, size_t> g_guarded;  // ptr -> requested bytes
+static int64_t g_guard_violations = 0;
+
+static void guard_check(void* p, size_t bytes) {
+  std::vector<unsigned char> h(kGuard);
+  cudaDeviceSynchronize();
+  if (cudaMemcpy(h.data(), (char*)p + bytes, kGuard, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  for (size_t i = 0; i < kGuard; ++i)
+    if (h[i] != kCanary) {
+      fprintf(stderr, "[rcg guard] write past the end of a %zu-byte pool buffer at +%zu bytes\n", bytes, i);
+      ++g_guard_violations;
+      if (getenv("RCG_POOL_GUARD_ABORT")) abort();
+      return;
+    }
+}
+
+extern "C" int64_t rcg_debug_guard_violations() {
+  std::lock_guard<std::mutex> g(g_guard_mu);
+  for (auto& kv : g_guarded) guard_check(kv.first, kv.second);
+  return g_guard_violations;
+}
+
+static void* guard_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes + kGuard) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  cudaDeviceSynchronize();
+  cudaMemset((char*)p + bytes, kCanary, kGuard);
+  cudaDeviceSynchronize();
+  std::lock_guard<std::mutex> g(g_guard_mu);
+  g_guarded[p] = bytes;
+  return p;
+}
+
+static void guard_release(void* p) {
+  std::lock_guard<std::mutex> g(g_guard_mu);
+  auto it = g_guarded.find(p);
+  if (it != g_guarded.end()) {
+    guard_check(p, it->second);
+    g_guarded.erase(it);
+  }
+  cudaFree(p);
+}
+
 void* Pool::get(size_t bytes) {
+  if (pool_guard()) return guard_alloc(bytes);
+  if (pool_exact()) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes ? bytes : 1) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    return p;
+  }
   bytes = (bytes + 4095) & ~(size_t)4095;
   {
     std::lock_guard<std::mutex> g(mu);
@@ -73,6 +170,14 @@ void* Pool::get(size_t bytes) {
 
 void Pool::put(void* p, size_t bytes) {
   if (!p) return;
+  if (pool_guard()) {
+    guard_release(p);
+    return;
+  }
+  if (pool_exact()) {
+    cudaFree(p);
+    return;
+  }
   bytes = (bytes + 4095) & ~(size_t)4095;
   std::lock_guard<std::mutex> g(mu);
   free_.emplace(bytes, p);
@@ -190,7 +295,10 @@ extern "C" void rcg_ctx_destroy(rcg_ctx* c) {
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.second.first);
   if (c->dargs) cudaFree(c->dargs);
   if (c->capture_stream) cudaStreamDestroy(c->capture_stream);
-  if (c->scratch) cudaFree(c->scratch);
+  if (c->scratch) {
+    if (pool_guard()) guard_release(c->scratch);
+    else cudaFree(c->scratch);
+  }
   if (c->counters) cudaFree(c->counters);
   if (c->pinned) cudaFreeHost(c->pinned);
   for (auto& p : c->pending) {

@@ -115,3 +115,20 @@ def test_device_tensors_pass_through(rng):
                            rcg.SolveConfig(tol=1e-10))
     assert isinstance(x, torch.Tensor) and x.is_cuda
     np.testing.assert_allclose((A @ x.cpu().numpy()), b.cpu().numpy(), atol=1e-8 * float(b.norm()))
+
+
+def test_no_pool_buffer_overruns_under_guard():
+    """Every solve-path kernel variant (BSR3 / CSR SpMV, SRKS / TRKS, reorth
+    on / off, krylov_cap, the n_c > 64 coarse kernel) run with guarded pool
+    and scratch buffers (RCG_POOL_GUARD: canary zone behind every buffer,
+    checked on release): no kernel writes past the end of its buffers."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, RCG_POOL_GUARD="1")
+    out = subprocess.run([sys.executable, str(root / "tools" / "memcheck_seq.py")], env=env, cwd=root,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "GUARD_VIOLATIONS 0" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]

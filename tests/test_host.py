@@ -17,7 +17,7 @@ REPO = Path(__file__).resolve().parents[1]
 def test_library_exports_every_header_symbol():
     lib = _lib.load()
     header = (REPO / "include" / "rcg.h").read_text()
-    declared = set(re.findall(r"^\s*(?:int|void|const char\*)\s+(rcg_\w+)\s*\(", header, flags=re.M))
+    declared = set(re.findall(r"^\s*(?:int|int64_t|void|const char\*)\s+(rcg_\w+)\s*\(", header, flags=re.M))
     assert declared, "no declarations parsed"
     assert declared == set(_lib.EXPORTS), declared ^ set(_lib.EXPORTS)
     for name in declared:
