@@ -81,37 +81,72 @@ struct IterArgs {
 // (base, ld and the tile start are 16-B aligned), so a lane keeps CG
 // LDG.128 in flight per step and reuses each smem vector element for CG
 // columns.  Slice partials are combined in smem in a fixed order.
-template <int CG, int NV>
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// With `pf`, lanes 0..CG-1 keep the bulk-copy engine PF_DIST steps (x 512 B)
+// ahead of the warp's own loads: every PF_WIN steps each issues one
+// cp.async.bulk.prefetch.L2 of PF_WIN x 512 B of its column.  The register-
+// limited K3 (2 CTAs/SM) gets HBM requests in flight without holding
+// registers: 5.86 -> 6.4 TB/s in tools/gemv_layout_bench3.cu.
+constexpr int PF_DIST = 2, PF_WIN = 4;
+
+// GEMV-T of one row tile: out[k*NV + v] = sum_rows M[:, k] v_v for k < ncols.
+// Items are (column group, row slice) pairs taken round-robin by the warps;
+// the slice count S is uniform per round.  Whole rounds run one group per
+// warp (S = 1); the r < kWarps leftover groups then run split kWarps ways
+// (one group per round), so no warp idles at the CTA's final barrier through
+// a whole extra item (j ~ 600: 75 groups = 9 rounds + 3/8).  With few groups
+// (< kWarps) S is the power of two that gives every warp an item.  The S
+// slices of a group are consecutive warps of one round and are combined in
+// smem in slice order (deterministic).
+template <int CG, int NV, bool PF = false>
 __device__ __forceinline__ void gemv_t_tile(const double* __restrict__ base, int64_t ld, int64_t ncols, int64_t len,
                                             const double* __restrict__ v0, const double* __restrict__ v1,
                                             double* __restrict__ out, double* __restrict__ red /* smem kWarps*CG*NV */) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t ngroups = (ncols + CG - 1) / CG;
-  // row slices per group: enough items for every warp when groups are few
-  // (a power of two dividing kWarps, so the S slices of a group are always
-  // consecutive warps of the same round)
-  int S = 1;
-  while (S < kWarps && ngroups * S < kWarps) S *= 2;
   const int64_t pairs = len >> 1;  // full row pairs
-  const int64_t per = (pairs + S - 1) / S;
-  const int64_t nitems = ngroups * S;
-  for (int64_t rnd = 0; rnd * kWarps < nitems; ++rnd) {
-    const int64_t item = rnd * kWarps + wid;
+  int S0 = 1;
+  while (S0 < kWarps && ngroups * S0 < kWarps) S0 *= 2;
+  const int64_t main_rounds = ngroups >= kWarps ? ngroups / kWarps : (ngroups * S0 + kWarps - 1) / kWarps;
+  const int64_t tail_groups = ngroups >= kWarps ? ngroups - main_rounds * kWarps : 0;
+  const int64_t rounds = main_rounds + tail_groups;
+  for (int64_t rnd = 0; rnd < rounds; ++rnd) {
+    const bool tail = rnd >= main_rounds;
+    const int S = tail ? kWarps : S0;
+    const int64_t item = tail ? (main_rounds * kWarps + (rnd - main_rounds) * kWarps + wid)
+                              : rnd * kWarps + wid;  // tail: group main_groups + (rnd - main_rounds)
+    const int64_t nitems = tail ? (main_rounds * kWarps + tail_groups * kWarps) : ngroups * S0;
+    const int64_t per = (pairs + S - 1) / S;
     double a0[CG], a1[CG];
 #pragma unroll
     for (int c = 0; c < CG; ++c) a0[c] = a1[c] = 0.0;
     int64_t g = -1;
     int sl = 0;
     if (item < nitems) {
-      g = item / S;
-      sl = (int)(item % S);
+      g = tail ? main_rounds * kWarps + (rnd - main_rounds) : item / S;
+      sl = tail ? wid : (int)(item % S);
       const int64_t k0 = g * CG;
       const int kc = (int)min((int64_t)CG, ncols - k0);
       const double* __restrict__ cols = base + k0 * ld;
       const int64_t p_begin = sl * per, p_end = min(pairs, p_begin + per);
       if (kc == CG) {
+        if (PF && lane < CG && p_begin < p_end)
+          bulk_prefetch_l2(cols + lane * ld + 2 * p_begin,
+                           (unsigned)(16 * min((int64_t)32 * PF_DIST, p_end - p_begin)));
 #pragma unroll 2
         for (int64_t pi = p_begin + lane; pi < p_end; pi += 32) {
+          if (PF && lane < CG) {
+            const int64_t step0 = pi - lane - p_begin;  // multiple of 32
+            if ((step0 & (32 * PF_WIN - 1)) == 0) {
+              const int64_t ahead = p_begin + step0 + 32 * PF_DIST;
+              if (ahead < p_end)
+                bulk_prefetch_l2(cols + lane * ld + 2 * ahead,
+                                 (unsigned)(16 * min((int64_t)32 * PF_WIN, p_end - ahead)));
+            }
+          }
           const double2 x0 = *reinterpret_cast<const double2*>(v0 + 2 * pi);
           double2 x1 = make_double2(0.0, 0.0);
           if (NV == 2) x1 = *reinterpret_cast<const double2*>(v1 + 2 * pi);
@@ -338,8 +373,8 @@ coarse_kernel(const IterArgs* __restrict__ ap, int check_done) {
 // ---------------------------------------------------------------------------
 // K3: convergence test, z = M^{-1} r - C s, (r, z), reorth partials
 
-template <int CG>
-__global__ void __launch_bounds__(kThreads)
+template <int CG, bool PF>
+__global__ void __launch_bounds__(kThreads, 2)
 precond_kernel(const IterArgs* __restrict__ ap, int init) {
   const IterArgs& a = *ap;
   SolveState* st = a.st;
@@ -415,8 +450,8 @@ precond_kernel(const IterArgs* __restrict__ ap, int init) {
     // AW is fully stored when reorthogonalizing (mod 0): column k at base + k*ld
     __shared__ double red[kWarps * CG * 2];
     const long long kb = (j + 1) * split / S, ke = (j + 1) * (split + 1) / S;
-    gemv_t_tile<CG, 2>(a.AW.base + kb * a.AW.ld + r0, a.AW.ld, ke - kb, r1 - r0, ztile, wtile,
-                      a.part_reo + (size_t)blockIdx.x * a.reo_stride + 2 * kb, red);
+    gemv_t_tile<CG, 2, PF>(a.AW.base + kb * a.AW.ld + r0, a.AW.ld, ke - kb, r1 - r0, ztile, wtile,
+                          a.part_reo + (size_t)blockIdx.x * a.reo_stride + 2 * kb, red);
   }
   if (lead && arrive_last(a.counters + 2)) reduce_partials<kThreads>(a.part_z, gridDim.x, 1, a.sums + a.rz_off);
 }
@@ -490,13 +525,27 @@ wupdate_kernel(const IterArgs* __restrict__ ap) {
         cp[k] = (red[2 * kk] + beta * red[2 * kk + 1]) / a.waw_diag[kk];
       }
       __syncthreads();
+      // reorth implies a stored W history (ColSel mod == 0): column k at base + k ld
+      const double* col0 = a.W.base + (k0 + a.W.shift) * a.W.ld + r0 + threadIdx.x;
+      const int64_t ldw = a.W.ld;
+      if (r0 + (int64_t)kThreads * RPT <= a.n) {
+        // full row block: RPT x 4 independent loads in flight per thread
 #pragma unroll 4
-      for (long long k = 0; k < kn; ++k) {
-        const double* col = a.W.at(k0 + k) + r0 + threadIdx.x;
-        const double ck = cp[k];
+        for (long long k = 0; k < kn; ++k) {
+          const double* col = col0 + k * ldw;
+          const double ck = cp[k];
 #pragma unroll
-        for (int q = 0; q < RPT; ++q)
-          if (r0 + threadIdx.x + q * kThreads < a.n) acc[q] += col[q * kThreads] * ck;
+          for (int q = 0; q < RPT; ++q) acc[q] += __ldcs(col + q * kThreads) * ck;
+        }
+      } else {
+#pragma unroll 4
+        for (long long k = 0; k < kn; ++k) {
+          const double* col = col0 + k * ldw;
+          const double ck = cp[k];
+#pragma unroll
+          for (int q = 0; q < RPT; ++q)
+            if (r0 + threadIdx.x + q * kThreads < a.n) acc[q] += col[q * kThreads] * ck;
+        }
       }
     }
   }
@@ -869,7 +918,12 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   // K5 rows per thread: 4, or 16 when that keeps the grid below 8 CTAs/SM
   // (n ~ 1e7: fewer last-block arrivals on one counter)
   // (without reorth only: the 16-row variant is slow on the W GEMV)
-  const int wu_rpt = (!reorth && ceil_div(n, (int64_t)kThreads * WU_RPT) > 8 * c->num_sms) ? 16 : WU_RPT;
+  // rows per thread: 8 with reorth (8 rows x 4 unrolled columns = 32 loads in
+  // flight per thread: 0.96 of copy bandwidth vs 0.78 for 4 rows,
+  // tools/gemv_layout_bench3.cu); RCG_WU_RPT=4 restores the old shape
+  static const int wu_rpt_env = env_int("RCG_WU_RPT", 8) == 4 ? 4 : 8;
+  const int wu_rpt = (!reorth && ceil_div(n, (int64_t)kThreads * WU_RPT) > 8 * c->num_sms) ? 16
+                     : (reorth ? wu_rpt_env : WU_RPT);
   const int wu_grid = (int)std::max<int64_t>(1, ceil_div(n, (int64_t)kThreads * wu_rpt));
   // launch grids: the tile kernels grid-stride, capped at a few CTAs per SM
   const int cap_grid = 8 * c->num_sms;
@@ -1021,7 +1075,10 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   RCG_CUDA(c, cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(smem_upd, 1024)));
   static const int pre_cg = env_int("RCG_PRE_CG", 8);
-  auto pre = pre_cg == 4 ? precond_kernel<4> : (pre_cg == 2 ? precond_kernel<2> : precond_kernel<8>);
+  static const bool pre_pf = env_int("RCG_PF", 1) != 0;
+  auto pre = pre_cg == 4 ? precond_kernel<4, false>
+                         : (pre_cg == 2 ? precond_kernel<2, false>
+                                        : (pre_pf ? precond_kernel<8, true> : precond_kernel<8, false>));
   RCG_CUDA(c, cudaFuncSetAttribute(pre, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(smem_pre, 1024)));
 
@@ -1177,6 +1234,8 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
       if (direct) prof_begin(c, RCG_K_WUPDATE, 8.0 * nd * (3 + (reorth ? js : 0.0)));
       if (wu_rpt == 16)
         wupdate_kernel<16><<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
+      else if (wu_rpt == 8)
+        wupdate_kernel<8><<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
       else
         wupdate_kernel<WU_RPT><<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
       RCG_LAUNCH_CHECK(c);
