@@ -64,6 +64,12 @@ typedef struct {
   const int32_t* bsr_row_offsets;   /* [n/3 + 1] block-row offsets (blocks)   */
   const int32_t* bsr_col_indices;   /* [nnz/9]   block column indices         */
   const double* bsr_values;         /* [nnz]     9 per block, row-major       */
+  int32_t bsr_slice;                /* 0 = plain BSR above; 32 = sliced (SELL-32
+                                       over block rows): bsr_row_offsets holds
+                                       [ceil(n/96)+1] chunk slot offsets,
+                                       bsr_col_indices [32*slots] (-1 = pad),
+                                       bsr_values [288*slots] */
+  int32_t pad0;
 } rcg_csr;
 
 /* Deflation operator P = I - C G^{-1} (AC)^T, G = C^T A C (DeflationOperator,
@@ -199,6 +205,31 @@ int rcg_csr_diagonal(rcg_ctx* ctx, const rcg_csr* A, double* diag, double* inv_d
 int rcg_csr_block3_analyze(rcg_ctx* ctx, const rcg_csr* A, int32_t* is_block3_host);
 /* Build the 3x3 BSR copy: bro[n/3+1], bci[nnz/9], bval[nnz]. */
 int rcg_csr_block3_build(rcg_ctx* ctx, const rcg_csr* A, int32_t* bro, int32_t* bci, double* bval);
+/* Sliced 3x3 blocks from a plain BSR operator (A->block == 3, bsr_slice == 0):
+ * plan writes chunk_offsets[ceil(n/96)+1] (device) and the slot count
+ * (synchronizes); build fills sci[32*slots], sval[288*slots].  The result is
+ * used by setting bsr_row_offsets/col_indices/values to these arrays and
+ * bsr_slice = 32. */
+int rcg_csr_block3_slice_plan(rcg_ctx* ctx, const rcg_csr* A, int32_t* chunk_offsets, int64_t* slots_host);
+int rcg_csr_block3_slice_build(rcg_ctx* ctx, const rcg_csr* A, const int32_t* chunk_offsets,
+                               int32_t* sci, double* sval);
+/* ---- device assembly of the BASELINE operators (problems.py) -------------- */
+/* Structured FD diffusion with harmonic face means and Dirichlet faces
+ * (_assemble_diffusion, /root/reference/pkg/src/recycg/problems.py:115-156),
+ * cells row-major over dims[0..ndim) (ndim 1..3).  rows: ro64[n+1] gets the
+ * int64 row offsets, *nnz_host the entry count (synchronizes).  fill: column
+ * indices, values and (ro32 != NULL) an int32 copy of the offsets; the bytes
+ * equal the host assembler's (problems.py:assemble_diffusion). */
+int rcg_gen_diffusion_rows(rcg_ctx* ctx, const int64_t* dims, int32_t ndim, int64_t* ro64, int64_t* nnz_host);
+int rcg_gen_diffusion_fill(rcg_ctx* ctx, const int64_t* dims, int32_t ndim, const double* coeff,
+                           const int64_t* ro64, int32_t* ro32, int32_t* ci, double* va);
+/* Q1 hex elasticity on nelem^3 elements, face x = 0 clamped (problems.py:
+ * elasticity_q1; no reference generator exists).  Ke: the 24x24 element
+ * stiffness at E = 1 (row-major, device); E: nelem^3 per-element moduli
+ * [ex][ey][ez] (device) or NULL for E = 1. */
+int rcg_gen_elasticity_rows(rcg_ctx* ctx, int64_t nelem, int64_t* ro64, int64_t* nnz_host);
+int rcg_gen_elasticity_fill(rcg_ctx* ctx, int64_t nelem, const double* Ke, const double* E,
+                            const int64_t* ro64, int32_t* ro32, int32_t* ci, double* va);
 /* elementwise y = inv_diag * x (Preconditioner.apply, solver.py:50-54) */
 int rcg_diag_apply(rcg_ctx* ctx, int64_t n, const double* inv_diag, const double* x, double* y);
 

@@ -13,7 +13,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "librcg.so"
-SOURCES = ["api.cu", "spmv.cu", "dense.cu", "pcg.cu", "ritz.cu", "comm.cu", "vmm.cu"]
+SOURCES = ["api.cu", "spmv.cu", "dense.cu", "pcg.cu", "ritz.cu", "comm.cu", "vmm.cu", "gen.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -29,7 +29,8 @@ class RcgCsr(C.Structure):
     _fields_ = [("n", C.c_int64), ("nnz", C.c_int64), ("row_offsets", C.c_void_p),
                 ("row_offsets_64", C.c_int32), ("block", C.c_int32),
                 ("col_indices", C.c_void_p), ("values", C.c_void_p),
-                ("bsr_row_offsets", C.c_void_p), ("bsr_col_indices", C.c_void_p), ("bsr_values", C.c_void_p)]
+                ("bsr_row_offsets", C.c_void_p), ("bsr_col_indices", C.c_void_p), ("bsr_values", C.c_void_p),
+                ("bsr_slice", C.c_int32), ("pad0", C.c_int32)]
 
 
 class RcgDeflation(C.Structure):
@@ -95,6 +96,12 @@ SIGNATURES = {
     "rcg_csr_diagonal": (C.c_int, [_vp, C.POINTER(RcgCsr), _vp, _vp]),
     "rcg_csr_block3_analyze": (C.c_int, [_vp, C.POINTER(RcgCsr), C.POINTER(_i32)]),
     "rcg_csr_block3_build": (C.c_int, [_vp, C.POINTER(RcgCsr), _vp, _vp, _vp]),
+    "rcg_gen_diffusion_rows": (C.c_int, [_vp, _vp, C.c_int32, _vp, C.POINTER(C.c_int64)]),
+    "rcg_gen_diffusion_fill": (C.c_int, [_vp, _vp, C.c_int32, _vp, _vp, _vp, _vp, _vp]),
+    "rcg_gen_elasticity_rows": (C.c_int, [_vp, C.c_int64, _vp, C.POINTER(C.c_int64)]),
+    "rcg_gen_elasticity_fill": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "rcg_csr_block3_slice_plan": (C.c_int, [_vp, C.POINTER(RcgCsr), _vp, C.POINTER(C.c_int64)]),
+    "rcg_csr_block3_slice_build": (C.c_int, [_vp, C.POINTER(RcgCsr), _vp, _vp, _vp]),
     "rcg_diag_apply": (C.c_int, [_vp, _i64, _vp, _vp, _vp]),
     "rcg_gemm_tn": (C.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i32]),
     "rcg_gemm_nn": (C.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64]),

@@ -104,7 +104,29 @@ class _DevCsr:
         self.struct.bsr_col_indices = self.bci.data_ptr()
         self.struct.bsr_values = self.bval.data_ptr()
         self.struct.block = 3
+        if _os.environ.get("RCG_SELL", "1") != "0":
+            self._slice(ctx)
         return True
+
+    def _slice(self, ctx):
+        """Re-lay the BSR copy as 32-row slices (SELL-32 over block rows,
+        spmv.cu ``sell3_body``) and drop the plain BSR arrays."""
+        torch = _torch()
+        nchunks = (int(self.struct.n) // 3 + 31) // 32
+        off = torch.empty(nchunks + 1, dtype=torch.int32, device="cuda")
+        slots = _lib.C.c_int64(0)
+        ctx.check(ctx.lib.rcg_csr_block3_slice_plan(ctx.h, _lib.C.byref(self.struct), _lib.ptr(off),
+                                                    _lib.C.byref(slots)), "block3_slice_plan")
+        sci = torch.empty(max(32 * slots.value, 1), dtype=torch.int32, device="cuda")
+        sval = torch.empty(max(288 * slots.value, 1), dtype=torch.float64, device="cuda")
+        ctx.check(ctx.lib.rcg_csr_block3_slice_build(ctx.h, _lib.C.byref(self.struct), _lib.ptr(off),
+                                                     _lib.ptr(sci), _lib.ptr(sval)), "block3_slice_build")
+        torch.cuda.synchronize()  # the plain BSR arrays are released below
+        self.bro, self.bci, self.bval = off, sci, sval
+        self.struct.bsr_row_offsets = off.data_ptr()
+        self.struct.bsr_col_indices = sci.data_ptr()
+        self.struct.bsr_values = sval.data_ptr()
+        self.struct.bsr_slice = 32
 
 
 @dataclass(frozen=True, eq=False)
@@ -206,8 +228,7 @@ class SparseSpdMatrix:
             ci = torch.from_numpy(np.ascontiguousarray(self.col_indices, dtype=np.int32)).to("cuda")
             va = torch.from_numpy(self.values).to("cuda")
             h = _DevCsr(ro, ci, va, self.n, self.nnz, ro64)
-            if self.use_block3 and _os.environ.get("RCG_BSR", "1") != "0" and self.n % 3 == 0 and self.nnz % 9 == 0 and self.nnz >= 9 * self.n // 3 * 2:
-                h.add_block3(_lib.context())
+            _maybe_block3(h, self.n, self.nnz, self.use_block3)
             self._dev[dev] = h
         return h
 
@@ -258,6 +279,57 @@ class SparseSpdMatrix:
                                        self.n), "spmm")
             return Y.cpu().numpy().T.copy() if host else Y.t()
         raise ContractViolation("operand must be a vector or an (n, k) block")
+
+
+def _maybe_block3(h, n, nnz, use_block3):
+    if use_block3 and _os.environ.get("RCG_BSR", "1") != "0" and n % 3 == 0 and nnz % 9 == 0 and nnz >= 9 * n // 3 * 2:
+        h.add_block3(_lib.context())
+
+
+class DeviceSparseSpdMatrix(SparseSpdMatrix):
+    """A ``SparseSpdMatrix`` assembled directly in HBM (``problems.py`` device
+    generators, ``csrc/gen.cu``).  The device CSR is the primary copy; the
+    host arrays (``row_offsets``, ``col_indices``, ``values``) are downloaded
+    on first access, so oracle checks and host-side code still see the
+    reference's CSR container."""
+
+    def __init__(self, n, dev_csr, device, use_block3=True):  # noqa: D107 (frozen dataclass: set via object)
+        object.__setattr__(self, "n", int(n))
+        object.__setattr__(self, "validate", False)
+        object.__setattr__(self, "use_block3", use_block3)
+        object.__setattr__(self, "_dev", {device: dev_csr})
+        object.__setattr__(self, "_nnz", int(dev_csr.struct.nnz))
+        object.__setattr__(self, "_host", None)
+        _maybe_block3(dev_csr, self.n, self._nnz, use_block3)
+
+    def _host_arrays(self):
+        if self._host is None:
+            h = next(iter(self._dev.values()))
+            ro = h.ro.cpu().numpy().astype(np.int64)
+            ci = h.ci.cpu().numpy()
+            va = h.va.cpu().numpy()
+            object.__setattr__(self, "_host", (ro, ci, va))
+        return self._host
+
+    @property
+    def row_offsets(self):
+        return self._host_arrays()[0]
+
+    @property
+    def col_indices(self):
+        return self._host_arrays()[1]
+
+    @property
+    def values(self):
+        return self._host_arrays()[2]
+
+    @property
+    def nnz(self):
+        return self._nnz
+
+    def release_device(self):
+        self._host_arrays()
+        self._dev.clear()
 
 
 def spmv(A: SparseSpdMatrix, x):

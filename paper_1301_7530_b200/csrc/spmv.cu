@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #ifndef RCG_SPMV_MINB
 #define RCG_SPMV_MINB 4
@@ -216,6 +217,154 @@ __device__ __forceinline__ void bsr3_body(int64_t nbr, const int32_t* __restrict
     if (K == 2) part[(size_t)blockIdx.x * K + 1] = t1;
   }
   if (arrive_last(counter)) reduce_partials<kThreads>(part, gridDim.x, K, out);
+}
+
+// ---------------------------------------------------------------------------
+// Sliced 3x3 blocks (SELL-32 over block rows): lane l of a warp owns block
+// row 32c + l of chunk c and walks its blocks in column order.  Slot k of
+// chunk c holds the k-th block of each of the 32 block rows side by side:
+// index at 32*s + l, value q at 32*(9*s + q) + l (s = chunk_offsets[c] + k),
+// so every index and value load of the warp is one contiguous 128/256-byte
+// access, no lane idles on a shuffle, and (for grid-numbered FEM meshes)
+// neighbouring lanes gather neighbouring x triples.  Short block rows are
+// padded to the chunk's widest with index -1 (value 0, gather skipped).
+// Row sums accumulate block by block in column order:
+//   y_i += (v_i0 x_0 + v_i1 x_1) + v_i2 x_2.
+
+template <int MODE, int U>
+__device__ __forceinline__ void sell3_body(int64_t nbr, const int32_t* __restrict__ off,
+                                           const int32_t* __restrict__ sci, const double* __restrict__ sv,
+                                           const ColSel& xs, const ColSel& ys, const double* __restrict__ b,
+                                           const SolveState* st, double* part, unsigned int* counter, double* out) {
+  long long j = 0;
+  if (st) {
+    if (st->done) return;
+    j = st->j;
+  }
+  const double* __restrict__ x = xs.at(j);
+  double* __restrict__ y = ys.at(j);
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nchunks = (nbr + 31) >> 5;
+  double d0 = 0.0, d1 = 0.0;
+  for (int64_t c = warp; c < nchunks; c += nwarps) {
+    const int64_t s0 = __ldg(off + c), s1 = __ldg(off + c + 1);
+    const int32_t* __restrict__ ip = sci + 32 * s0 + lane;
+    const double* __restrict__ vp = sv + 32 * 9 * s0 + lane;
+    const int w = (int)(s1 - s0);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int k = 0; k < w; k += U) {
+      int ci[U];
+      double v[U][9];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool ok = k + u < w;
+        ci[u] = ok ? __ldcs(ip + 32 * (k + u)) : -1;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) v[u][q] = ok ? __ldcs(vp + 32 * (9 * (k + u) + q)) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (ci[u] >= 0) {
+          const double* xc = x + 3 * (int64_t)ci[u];
+          const double x0 = __ldg(xc), x1 = __ldg(xc + 1), x2 = __ldg(xc + 2);
+          a0 += (v[u][0] * x0 + v[u][1] * x1) + v[u][2] * x2;
+          a1 += (v[u][3] * x0 + v[u][4] * x1) + v[u][5] * x2;
+          a2 += (v[u][6] * x0 + v[u][7] * x1) + v[u][8] * x2;
+        }
+      }
+    }
+    const int64_t p = 32 * c + lane;
+    if (p < nbr) {
+      const int64_t r = 3 * p;
+      if (MODE == 2) {
+        const double b0 = b[r], b1 = b[r + 1], b2 = b[r + 2];
+        a0 = b0 - a0;
+        a1 = b1 - a1;
+        a2 = b2 - a2;
+        d1 += (b0 * b0 + b1 * b1) + b2 * b2;
+        d0 += (a0 * a0 + a1 * a1) + a2 * a2;
+      } else if (MODE == 1) {
+        d0 += (x[r] * a0 + x[r + 1] * a1) + x[r + 2] * a2;
+      }
+      y[r] = a0;
+      y[r + 1] = a1;
+      y[r + 2] = a2;
+    }
+  }
+  if (MODE == 0) return;
+  __shared__ double sm[kWarps];
+  const double t0 = block_sum<kThreads>(d0, sm);
+  double t1 = 0.0;
+  if (MODE == 2) t1 = block_sum<kThreads>(d1, sm);
+  constexpr int K = MODE == 2 ? 2 : 1;
+  if (threadIdx.x == 0) {
+    part[(size_t)blockIdx.x * K] = t0;
+    if (K == 2) part[(size_t)blockIdx.x * K + 1] = t1;
+  }
+  if (arrive_last(counter)) reduce_partials<kThreads>(part, gridDim.x, K, out);
+}
+
+#ifndef RCG_SELL_U
+#define RCG_SELL_U 1
+#endif
+#ifndef RCG_SELL_MINB
+#define RCG_SELL_MINB 4
+#endif
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, RCG_SELL_MINB)
+sell3_kernel(int64_t nbr, const int32_t* __restrict__ off, const int32_t* __restrict__ sci,
+             const double* __restrict__ sv, ColSel xs, ColSel ys, const double* __restrict__ b,
+             const SolveState* st, double* part, unsigned int* counter, double* out) {
+  sell3_body<MODE, RCG_SELL_U>(nbr, off, sci, sv, xs, ys, b, st, part, counter, out);
+}
+
+__global__ void __launch_bounds__(kThreads, RCG_SELL_MINB) sell3_kernel_ind(const SpmvArgs* __restrict__ sa) {
+  sell3_body<1, RCG_SELL_U>(sa->n / 3, sa->bro, sa->bci, sa->bval, sa->xs, sa->ys, nullptr, sa->st, sa->part,
+                            sa->counter, sa->out);
+}
+
+int sell3_grid(Ctx* c, int64_t nbr) {
+  static const int ctas = [] {
+    const char* e = getenv("RCG_SELL_CTAS");
+    return e ? std::max(1, atoi(e)) : 8;   // sweep (tools/sweep_sell.sh): U=1, 4 resident, 8/SM grid best
+  }();
+  const int64_t g = ceil_div(ceil_div(nbr, 32), kWarps);
+  const int64_t cap = (int64_t)c->num_sms * ctas;
+  return (int)std::max<int64_t>(1, std::min(g, cap));
+}
+
+// chunk widths (max blocks per block row over each 32-row chunk) from plain BSR
+__global__ void sell3_width_kernel(int64_t nbr, const int32_t* __restrict__ bro, int32_t* widths) {
+  const int64_t nchunks = (nbr + 31) >> 5;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    int w = 0;
+    const int64_t pe = 32 * c + 32 < nbr ? 32 * c + 32 : nbr;
+    for (int64_t p = 32 * c; p < pe; ++p) w = max(w, bro[p + 1] - bro[p]);
+    widths[c] = w;
+  }
+}
+
+// scatter plain BSR (q-major within a block row) into the sliced layout
+__global__ void sell3_fill_kernel(int64_t nbr, const int32_t* __restrict__ bro, const int32_t* __restrict__ bci,
+                                  const double* __restrict__ bval, const int32_t* __restrict__ off,
+                                  int32_t* __restrict__ sci, double* __restrict__ sv) {
+  const int64_t nchunks = (nbr + 31) >> 5;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < 32 * nchunks;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = p >> 5, l = p & 31;
+    const int64_t s0 = off[c], w = off[c + 1] - s0;
+    const int64_t b0 = p < nbr ? bro[p] : 0, nb = p < nbr ? bro[p + 1] - b0 : 0;
+    for (int64_t k = 0; k < w; ++k) {
+      const int64_t s = s0 + k;
+      sci[32 * s + l] = k < nb ? bci[b0 + k] : -1;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) sv[32 * (9 * s + q) + l] = k < nb ? bval[9 * b0 + q * nb + k] : 0.0;
+    }
+  }
 }
 
 template <typename RO, int V, int MODE>
@@ -422,8 +571,27 @@ static void launch_v(int V, int grid, cudaStream_t s, const rcg_csr* A, ColSel x
 #undef RCG_SPMV_CASE
 }
 
+static inline bool is_sell3(const rcg_csr* A) {
+  return A->block == 3 && A->bsr_slice == 32 && A->bsr_row_offsets;
+}
+
 int launch_spmv(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const double* b,
                 const SolveState* st, double* part, unsigned int* counter, double* out) {
+  if (is_sell3(A)) {
+    const int64_t nbr = A->n / 3;
+    const int g = sell3_grid(c, nbr);
+    if (mode == 0)
+      sell3_kernel<0><<<g, kThreads, 0, c->stream>>>(nbr, A->bsr_row_offsets, A->bsr_col_indices, A->bsr_values, xs,
+                                                     ys, b, st, part, counter, out);
+    else if (mode == 1)
+      sell3_kernel<1><<<g, kThreads, 0, c->stream>>>(nbr, A->bsr_row_offsets, A->bsr_col_indices, A->bsr_values, xs,
+                                                     ys, b, st, part, counter, out);
+    else
+      sell3_kernel<2><<<g, kThreads, 0, c->stream>>>(nbr, A->bsr_row_offsets, A->bsr_col_indices, A->bsr_values, xs,
+                                                     ys, b, st, part, counter, out);
+    RCG_LAUNCH_CHECK(c);
+    return RCG_OK;
+  }
   if (A->block == 3 && A->bsr_row_offsets) {
     const int64_t nbr = A->n / 3;
     const int g = bsr3_grid(c, nbr);
@@ -455,6 +623,11 @@ int launch_spmv(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const 
 }
 
 int launch_spmv_ind(Ctx* c, const rcg_csr* A, const SpmvArgs* dargs) {
+  if (is_sell3(A)) {
+    sell3_kernel_ind<<<sell3_grid(c, A->n / 3), kThreads, 0, c->stream>>>(dargs);
+    RCG_LAUNCH_CHECK(c);
+    return RCG_OK;
+  }
   if (A->block == 3 && A->bsr_row_offsets) {
     bsr3_kernel_ind<<<bsr3_grid(c, A->n / 3), kThreads, 0, c->stream>>>(dargs);
     RCG_LAUNCH_CHECK(c);
@@ -503,6 +676,7 @@ void spmv_args_fill(const rcg_csr* A, SpmvArgs* s) {
 }
 
 int spmv_partials(Ctx* c, const rcg_csr* A) {
+  if (is_sell3(A)) return sell3_grid(c, A->n / 3);
   if (A->block == 3 && A->bsr_row_offsets) return bsr3_grid(c, A->n / 3);
   return spmv_grid(c, A, spmv_width(A));
 }
@@ -625,6 +799,47 @@ extern "C" int rcg_csr_block3_build(rcg_ctx* ctx, const rcg_csr* A, int32_t* bro
   else
     block3_build_kernel<int32_t><<<g, kThreads, 0, ctx->stream>>>(nbr, (const int32_t*)A->row_offsets,
                                                                   A->col_indices, A->values, bro, bci, bval);
+  RCG_LAUNCH_CHECK(ctx);
+  return RCG_OK;
+}
+
+extern "C" int rcg_csr_block3_slice_plan(rcg_ctx* ctx, const rcg_csr* A, int32_t* chunk_offsets,
+                                         int64_t* slots_host) {
+  if (!ctx || !A || !slots_host || !chunk_offsets) return RCG_ERR_CONTRACT;
+  if (A->block != 3 || A->bsr_slice != 0 || !A->bsr_row_offsets)
+    return set_error(ctx, RCG_ERR_CONTRACT, "slice_plan needs a plain 3x3 BSR operator");
+  const int64_t nbr = A->n / 3, nchunks = (nbr + 31) / 32;
+  std::vector<int32_t> h(nchunks + 1, 0);
+  if (nchunks > 0) {
+    sell3_width_kernel<<<elementwise_grid(ctx, nchunks), kThreads, 0, ctx->stream>>>(nbr, A->bsr_row_offsets,
+                                                                                      chunk_offsets + 1);
+    RCG_LAUNCH_CHECK(ctx);
+    RCG_CUDA(ctx, cudaMemcpyAsync(h.data() + 1, chunk_offsets + 1, nchunks * sizeof(int32_t),
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+    RCG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  int64_t acc = 0;
+  for (int64_t c = 1; c <= nchunks; ++c) {
+    acc += h[c];
+    if (acc >= ((int64_t)1 << 31) / (32 * 9)) return set_error(ctx, RCG_ERR_CONTRACT, "sliced BSR too large");
+    h[c] = (int32_t)acc;
+  }
+  RCG_CUDA(ctx, cudaMemcpyAsync(chunk_offsets, h.data(), (nchunks + 1) * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                ctx->stream));
+  RCG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  *slots_host = acc;
+  return RCG_OK;
+}
+
+extern "C" int rcg_csr_block3_slice_build(rcg_ctx* ctx, const rcg_csr* A, const int32_t* chunk_offsets,
+                                          int32_t* sci, double* sval) {
+  if (!ctx || !A || !chunk_offsets) return RCG_ERR_CONTRACT;
+  if (A->block != 3 || A->bsr_slice != 0 || !A->bsr_row_offsets)
+    return set_error(ctx, RCG_ERR_CONTRACT, "slice_build needs a plain 3x3 BSR operator");
+  const int64_t nbr = A->n / 3;
+  if (nbr == 0) return RCG_OK;
+  sell3_fill_kernel<<<elementwise_grid(ctx, 32 * ((nbr + 31) / 32)), kThreads, 0, ctx->stream>>>(
+      nbr, A->bsr_row_offsets, A->bsr_col_indices, A->bsr_values, chunk_offsets, sci, sval);
   RCG_LAUNCH_CHECK(ctx);
   return RCG_OK;
 }

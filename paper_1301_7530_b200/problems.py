@@ -131,6 +131,73 @@ def assemble_diffusion(cell_coeff, validate=None):
 
 
 # ---------------------------------------------------------------------------
+# device assemblers (csrc/gen.cu): same bytes as the host assemblers, built in
+# HBM; only the coefficient field crosses PCIe
+
+
+def _device_csr_from(rows_fn, fill_fn, n):
+    """Run a two-pass device assembler and wrap the CSR it writes."""
+    from ._lib import context, ptr, require_cuda, C
+    from .core import _DevCsr, DeviceSparseSpdMatrix
+    torch = require_cuda()
+    ctx = context()
+    ro64 = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    nnz = C.c_int64(0)
+    ctx.check(rows_fn(ctx, ptr(ro64), C.byref(nnz)), "gen rows")
+    nnz = nnz.value
+    wide = nnz >= 2 ** 31 - 1
+    ro32 = None if wide else torch.empty(n + 1, dtype=torch.int32, device="cuda")
+    ci = torch.empty(max(nnz, 1), dtype=torch.int32, device="cuda")
+    va = torch.empty(max(nnz, 1), dtype=torch.float64, device="cuda")
+    ctx.check(fill_fn(ctx, ptr(ro64), None if wide else ptr(ro32), ptr(ci), ptr(va)), "gen fill")
+    torch.cuda.synchronize()
+    ro = ro64 if wide else ro32
+    del ro64
+    h = _DevCsr(ro, ci[:nnz], va[:nnz], n, nnz, wide)
+    return DeviceSparseSpdMatrix(n, h, torch.cuda.current_device())
+
+
+def assemble_diffusion_device(cell_coeff):
+    """``assemble_diffusion`` on the device: the same CSR bytes, written in HBM.
+    ``cell_coeff`` is a host array or a CUDA tensor (1-3 dimensions)."""
+    from ._lib import require_cuda, ptr, C
+    torch = require_cuda()
+    if torch.is_tensor(cell_coeff):
+        coeff = cell_coeff.to(device="cuda", dtype=torch.float64).contiguous()
+    else:
+        coeff = torch.from_numpy(np.ascontiguousarray(cell_coeff, dtype=np.float64)).to("cuda")
+    shape = tuple(coeff.shape)
+    if not 1 <= len(shape) <= 3:
+        raise ContractViolation("cell_coeff must have 1 to 3 dimensions")
+    dims = (C.c_int64 * len(shape))(*shape)
+    n = int(np.prod(shape))
+    return _device_csr_from(
+        lambda ctx, ro, nnz: ctx.lib.rcg_gen_diffusion_rows(ctx.h, dims, len(shape), ro, nnz),
+        lambda ctx, ro, ro32, ci, va: ctx.lib.rcg_gen_diffusion_fill(ctx.h, dims, len(shape), ptr(coeff), ro, ro32,
+                                                                     ci, va), n)
+
+
+def elasticity_q1_device(nelem, E=None, nu=0.3):
+    """``elasticity_q1`` on the device (same CSR bytes).  ``E``: None or a host
+    array / CUDA tensor of shape ``(nelem,)*3``."""
+    from ._lib import require_cuda, ptr
+    torch = require_cuda()
+    N = int(nelem)
+    Ke = torch.from_numpy(np.ascontiguousarray(_q1_element_stiffness(1.0 / N, nu))).to("cuda")
+    Ed = None
+    if E is not None:
+        if tuple(E.shape) != (N, N, N):
+            raise ContractViolation("E must have shape (nelem,)*3")
+        Ed = (E.to(device="cuda", dtype=torch.float64).contiguous() if torch.is_tensor(E)
+              else torch.from_numpy(np.ascontiguousarray(E, dtype=np.float64)).to("cuda"))
+    n = 3 * N * (N + 1) * (N + 1)
+    return _device_csr_from(
+        lambda ctx, ro, nnz: ctx.lib.rcg_gen_elasticity_rows(ctx.h, N, ro, nnz),
+        lambda ctx, ro, ro32, ci, va: ctx.lib.rcg_gen_elasticity_fill(ctx.h, N, ptr(Ke), None if Ed is None else ptr(Ed),
+                                                                      ro, ro32, ci, va), n)
+
+
+# ---------------------------------------------------------------------------
 # the reference's own inclusion benchmark (problems.py:22-189)
 
 
@@ -304,7 +371,7 @@ def shifted_laplacian_sequence(grid=128, count=10, seed=0, shift=0.05):
 
 
 def lognormal_diffusion_sequence(grid=256, count=20, seed=0, sigma=2.0,
-                                 noise_sigma=0.05):
+                                 noise_sigma=0.05, device=False):
     """Config 4: 7-point diffusion, kappa0 ~ lognormal(0, sigma) per cell,
     kappa^(k) = kappa0 * lognormal(0, noise) independent per k, b ~ N(0,1)
     drawn once.  Yields lazily (each matrix is ~1.4 GB at 256^3)."""
@@ -315,7 +382,7 @@ def lognormal_diffusion_sequence(grid=256, count=20, seed=0, sigma=2.0,
     b = rng.standard_normal(n)
     for _ in range(count):
         kappa = kappa0 * rng.lognormal(0.0, noise_sigma, shape)
-        yield assemble_diffusion(kappa, validate=False), b.copy()
+        yield (assemble_diffusion_device(kappa) if device else assemble_diffusion(kappa, validate=False)), b.copy()
 
 
 # ---------------------------------------------------------------------------
@@ -466,7 +533,7 @@ def elasticity_rhs(N, rng):
     return b.reshape(-1)
 
 
-def elasticity_sequence(nelem, count, seed=0, kind="fixed", nu=0.3):
+def elasticity_sequence(nelem, count, seed=0, kind="fixed", nu=0.3, device=False):
     """Configs 2/3/5.
 
     * ``kind="fixed"`` (config 2): E = 1, ``count`` independent traction RHS.
@@ -474,12 +541,13 @@ def elasticity_sequence(nelem, count, seed=0, kind="fixed", nu=0.3):
       centroid is within 0.03 k of the cube centre; b^(k) = b0 + 0.01 k N(0,1).
     * ``kind="lognormal_softening"`` (config 5): base E ~ lognormal(0,1) per
       element, then the config-3 softening sequence.
+    ``device=True`` assembles each operator in HBM (``elasticity_q1_device``).
     Yields lazily.
     """
     N = int(nelem)
     rng = _philox(seed)
     if kind == "fixed":
-        A = elasticity_q1(N, nu=nu)
+        A = elasticity_q1_device(N, nu=nu) if device else elasticity_q1(N, nu=nu)
         for _ in range(count):
             yield A, elasticity_rhs(N, rng)
         return
@@ -493,27 +561,27 @@ def elasticity_sequence(nelem, count, seed=0, kind="fixed", nu=0.3):
     for k in range(count):
         E = np.where(r <= 0.03 * k, E0 * (0.6 ** k), E0)
         b = b0 + 0.01 * k * rng.standard_normal(b0.shape[0])
-        yield elasticity_q1(N, E=E, nu=nu, validate=False), b
+        yield (elasticity_q1_device(N, E=E, nu=nu) if device else elasticity_q1(N, E=E, nu=nu, validate=False)), b
 
 
-def config_systems(config, reduced=False):
+def config_systems(config, reduced=False, device=False):
     """(systems iterable, settings dict) for BASELINE.json config 1..5.
 
     ``reduced`` swaps in the oracle-sized analogs: elasticity
-    16^3 / 24^3, diffusion 64^3.
+    16^3 / 24^3, diffusion 64^3.  ``device`` assembles configs 2-5 in HBM.
     """
     if config == 1:
         return shifted_laplacian_sequence(), dict(tol=1e-8, epsilon=1e-10, nc_limit=21)
     if config == 2:
         N = 16 if reduced else 64
-        return elasticity_sequence(N, 20, kind="fixed"), dict(tol=1e-8, epsilon=1e-10, nc_limit=61)
+        return elasticity_sequence(N, 20, kind="fixed", device=device), dict(tol=1e-8, epsilon=1e-10, nc_limit=61)
     if config == 3:
         N = 24 if reduced else 96
-        return elasticity_sequence(N, 15, kind="softening"), dict(tol=1e-8, epsilon=1e-10, nc_limit=81)
+        return elasticity_sequence(N, 15, kind="softening", device=device), dict(tol=1e-8, epsilon=1e-10, nc_limit=81)
     if config == 4:
         g = 64 if reduced else 256
-        return lognormal_diffusion_sequence(g, 20), dict(tol=1e-8, epsilon=1e-10, nc_limit=21)
+        return lognormal_diffusion_sequence(g, 20, device=device), dict(tol=1e-8, epsilon=1e-10, nc_limit=21)
     if config == 5:
         N = 16 if reduced else 160
-        return elasticity_sequence(N, 10, kind="lognormal_softening"), dict(tol=1e-8, epsilon=1e-10, nc_limit=101)
+        return elasticity_sequence(N, 10, kind="lognormal_softening", device=device), dict(tol=1e-8, epsilon=1e-10, nc_limit=101)
     raise ContractViolation(f"unknown config {config}")

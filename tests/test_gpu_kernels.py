@@ -165,7 +165,28 @@ def test_block3_spmv_matches_scalar_csr(rng):
     ya, yb = rcg.spmv(A, x), rcg.spmv(B, x)
     np.testing.assert_allclose(ya, yb, rtol=1e-13, atol=1e-13 * np.abs(yb).max())
     _spmv_close(A, x)
+    assert A.device_csr().struct.bsr_slice == 32        # sliced layout is the default
     # not block structured -> scalar path
     L0 = problems.assemble_diffusion(np.ones((6, 6)))
     L = rcg.SparseSpdMatrix(L0.n, L0.row_offsets, L0.col_indices, L0.values, validate=False, use_block3=True)
     assert L.device_csr().struct.block == 0
+
+
+@pytest.mark.parametrize("nelem", [1, 3, 7])
+def test_sliced_block3_matches_plain_bsr(rng, monkeypatch, nelem):
+    """SELL-32 sliced 3x3 blocks (padded short block rows, a ragged last
+    chunk: n/3 not a multiple of 32) compute the same product as the plain
+    BSR layout (identical per-row block order and rounding) and as scipy."""
+    E = np.exp(rng.standard_normal((nelem,) * 3))
+    A0 = problems.elasticity_q1(nelem, E=E)
+    mk = lambda: rcg.SparseSpdMatrix(A0.n, A0.row_offsets, A0.col_indices, A0.values, validate=False)
+    S = mk()
+    assert S.device_csr().struct.bsr_slice == 32
+    monkeypatch.setenv("RCG_SELL", "0")
+    P = mk()
+    assert P.device_csr().struct.block == 3 and P.device_csr().struct.bsr_slice == 0
+    for _ in range(3):
+        x = rng.standard_normal(A0.n)
+        ys, yp = rcg.spmv(S, x), rcg.spmv(P, x)
+        np.testing.assert_allclose(ys, yp, rtol=1e-14, atol=1e-14 * np.abs(yp).max())
+        _spmv_close(S, x)
