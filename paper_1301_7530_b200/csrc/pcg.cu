@@ -338,9 +338,9 @@ actr_kernel(const IterArgs* __restrict__ ap) {
   }
   // last CTA of the 2-D grid reduces the AC^T y columns over the tiles
   __shared__ bool last;
-  __threadfence();
-  __syncthreads();
+  __syncthreads();  // + thread-0 fence (cumulative), see arrive_last
   if (threadIdx.x == 0) {
+    __threadfence();
     const unsigned int prev = atomicAdd(a.counters + 3, 1u);
     last = (prev == gridDim.x * gridDim.y - 1);
     if (last) a.counters[3] = 0u;
@@ -558,9 +558,9 @@ wupdate_kernel(const IterArgs* __restrict__ ap) {
       const int64_t i = r0 + threadIdx.x + q * kThreads;
       if (i < a.n) a.part_wu[(int64_t)split * a.n + i] = acc[q];
     }
-    __threadfence();
-    __syncthreads();
+    __syncthreads();  // + thread-0 fence (cumulative), see arrive_last
     if (threadIdx.x == 0) {
+      __threadfence();
       unsigned int* cnt = a.counters + 16 + blockIdx.x;
       const unsigned int prev = atomicAdd(cnt, 1u);
       s_last = (prev == (unsigned)S - 1);
@@ -596,9 +596,9 @@ wupdate_kernel(const IterArgs* __restrict__ ap) {
   }
   // the grid's last block advances the iteration (all blocks arrive once)
   __shared__ bool g_last;
-  __threadfence();
-  __syncthreads();
+  __syncthreads();  // + thread-0 fence (cumulative), see arrive_last
   if (threadIdx.x == 0) {
+    __threadfence();
     const unsigned int prev = atomicAdd(a.counters + 4, 1u);
     g_last = (prev == gridDim.x * gridDim.y - 1);
     if (g_last) a.counters[4] = 0u;

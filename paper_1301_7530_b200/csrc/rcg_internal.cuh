@@ -135,11 +135,14 @@ __device__ __forceinline__ double block_sum(double v, double* sm /* >= NT/32 */)
 // Last-block-done: every block has written its K partials to part[blockIdx*K+k];
 // returns true in exactly one block (the last to arrive), after which that
 // block may read all partials.  The counter is reset by the last block.
+// The barrier orders every thread's partial writes before thread 0's fence
+// (fence.sc is cumulative), so only thread 0 fences: the other threads do not
+// stall on the completion of their own streaming stores.
 __device__ __forceinline__ bool arrive_last(unsigned int* counter) {
   __shared__ bool last;
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence();
     unsigned int prev = atomicAdd(counter, 1u);
     last = (prev == gridDim.x - 1);
     if (last) *counter = 0u;

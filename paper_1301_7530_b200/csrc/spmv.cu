@@ -231,14 +231,17 @@ __device__ __forceinline__ void bsr3_body(int64_t nbr, const int32_t* __restrict
 // Row sums accumulate block by block in column order:
 //   y_i += (v_i0 x_0 + v_i1 x_1) + v_i2 x_2.
 
+// Returns false when the solve is done (kernel must exit); the block
+// partials of (x, y) [and (b, b)] are left in d0 [d1] for spmv_epilogue, so
+// the epilogue's pointers are not held in registers across the stream loop.
 template <int MODE, int U>
-__device__ __forceinline__ void sell3_body(int64_t nbr, const int32_t* __restrict__ off,
+__device__ __forceinline__ bool sell3_body(int64_t nbr, const int32_t* __restrict__ off,
                                            const int32_t* __restrict__ sci, const double* __restrict__ sv,
                                            const ColSel& xs, const ColSel& ys, const double* __restrict__ b,
-                                           const SolveState* st, double* part, unsigned int* counter, double* out) {
+                                           const SolveState* st, double& d0, double& d1) {
   long long j = 0;
   if (st) {
-    if (st->done) return;
+    if (st->done) return false;
     j = st->j;
   }
   const double* __restrict__ x = xs.at(j);
@@ -247,7 +250,8 @@ __device__ __forceinline__ void sell3_body(int64_t nbr, const int32_t* __restric
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nchunks = (nbr + 31) >> 5;
-  double d0 = 0.0, d1 = 0.0;
+  d0 = 0.0;
+  d1 = 0.0;
   for (int64_t c = warp; c < nchunks; c += nwarps) {
     const int64_t s0 = __ldg(off + c), s1 = __ldg(off + c + 1);
     const int32_t* __restrict__ ip = sci + 32 * s0 + lane;
@@ -257,12 +261,15 @@ __device__ __forceinline__ void sell3_body(int64_t nbr, const int32_t* __restric
     for (int k = 0; k < w; k += U) {
       int ci[U];
       double v[U][9];
+      // one base pointer per step: the 9 value loads use immediate offsets
+      const int32_t* __restrict__ ik = ip + (int64_t)32 * k;
+      const double* __restrict__ vk = vp + (int64_t)288 * k;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const bool ok = k + u < w;
-        ci[u] = ok ? __ldcs(ip + 32 * (k + u)) : -1;
+        ci[u] = ok ? __ldcs(ik + 32 * u) : -1;
 #pragma unroll
-        for (int q = 0; q < 9; ++q) v[u][q] = ok ? __ldcs(vp + 32 * (9 * (k + u) + q)) : 0.0;
+        for (int q = 0; q < 9; ++q) v[u][q] = ok ? __ldcs(vk + 288 * u + 32 * q) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -293,6 +300,13 @@ __device__ __forceinline__ void sell3_body(int64_t nbr, const int32_t* __restric
       y[r + 2] = a2;
     }
   }
+  return true;
+}
+
+// block partials of the fused dot products -> part; the last block reduces
+template <int MODE>
+__device__ __forceinline__ void spmv_epilogue(double d0, double d1, double* part, unsigned int* counter,
+                                              double* out) {
   if (MODE == 0) return;
   __shared__ double sm[kWarps];
   const double t0 = block_sum<kThreads>(d0, sm);
@@ -307,7 +321,7 @@ __device__ __forceinline__ void sell3_body(int64_t nbr, const int32_t* __restric
 }
 
 #ifndef RCG_SELL_U
-#define RCG_SELL_U 1
+#define RCG_SELL_U 2
 #endif
 #ifndef RCG_SELL_MINB
 #define RCG_SELL_MINB 4
@@ -318,12 +332,15 @@ __global__ void __launch_bounds__(kThreads, RCG_SELL_MINB)
 sell3_kernel(int64_t nbr, const int32_t* __restrict__ off, const int32_t* __restrict__ sci,
              const double* __restrict__ sv, ColSel xs, ColSel ys, const double* __restrict__ b,
              const SolveState* st, double* part, unsigned int* counter, double* out) {
-  sell3_body<MODE, RCG_SELL_U>(nbr, off, sci, sv, xs, ys, b, st, part, counter, out);
+  double d0, d1;
+  if (sell3_body<MODE, RCG_SELL_U>(nbr, off, sci, sv, xs, ys, b, st, d0, d1))
+    spmv_epilogue<MODE>(d0, d1, part, counter, out);
 }
 
 __global__ void __launch_bounds__(kThreads, RCG_SELL_MINB) sell3_kernel_ind(const SpmvArgs* __restrict__ sa) {
-  sell3_body<1, RCG_SELL_U>(sa->n / 3, sa->bro, sa->bci, sa->bval, sa->xs, sa->ys, nullptr, sa->st, sa->part,
-                            sa->counter, sa->out);
+  double d0, d1;
+  if (sell3_body<1, RCG_SELL_U>(sa->n / 3, sa->bro, sa->bci, sa->bval, sa->xs, sa->ys, nullptr, sa->st, d0, d1))
+    spmv_epilogue<1>(d0, d1, sa->part, sa->counter, sa->out);
 }
 
 int sell3_grid(Ctx* c, int64_t nbr) {
@@ -724,6 +741,42 @@ using namespace rcg;
 extern "C" int rcg_spmv(rcg_ctx* ctx, const rcg_csr* A, const double* x, double* y) {
   if (!ctx || !A) return RCG_ERR_CONTRACT;
   if (A->n == 0) return RCG_OK;
+  static const int ind = [] {
+    const char* e = getenv("RCG_SPMV_IND");   // diagnostics: route through the solve-loop kernel
+    return e ? atoi(e) : 0;
+  }();
+  if (ind) {
+    // args staged once per (A, x, y) so repeated calls time the kernel alone
+    static const void* last[4] = {nullptr, nullptr, nullptr, nullptr};
+    const int np = spmv_partials(ctx, A);
+    char* sc = nullptr;
+    const size_t need = 4096 + sizeof(double) * (np + 8);
+    const bool same = last[0] == A->values && last[1] == x && last[2] == y && last[3] == ctx->scratch &&
+                      ctx->scratch_bytes >= need;
+    int rc = scratch(ctx, need, (void**)&sc);
+    if (rc) return rc;
+    if (same && ind == 2) {   // direct mode-1 launch with the same partial buffers
+      return launch_spmv(ctx, A, 1, colsel((double*)x), colsel(y), nullptr, nullptr, (double*)(sc + 4096),
+                         (unsigned int*)(sc + 2048), (double*)(sc + 3072));
+    }
+    if (same) return launch_spmv_ind(ctx, A, (const SpmvArgs*)sc);
+    last[0] = A->values;
+    last[1] = x;
+    last[2] = y;
+    last[3] = sc;
+    SpmvArgs h{};
+    spmv_args_fill(A, &h);
+    h.xs = colsel((double*)x);
+    h.ys = colsel(y);
+    h.st = (const SolveState*)(sc + 1024);
+    h.counter = (unsigned int*)(sc + 2048);
+    h.out = (double*)(sc + 3072);
+    h.part = (double*)(sc + 4096);
+    RCG_CUDA(ctx, cudaMemsetAsync(sc, 0, 4096, ctx->stream));
+    RCG_CUDA(ctx, cudaMemcpyAsync(sc, &h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
+    RCG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return launch_spmv_ind(ctx, A, (const SpmvArgs*)sc);
+  }
   return launch_spmv(ctx, A, 0, colsel((double*)x), colsel(y), nullptr, nullptr, nullptr, nullptr,
                      nullptr);
 }
