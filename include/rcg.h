@@ -159,12 +159,13 @@ int64_t rcg_debug_guard_violations(void);
  * ALGORITHMIC bytes (each operand touched once) are accounted.  Classes: */
 enum rcg_kclass {
   RCG_K_SPMV = 0,      /* K1: Aw = A w, (w, Aw)                         */
-  RCG_K_UPDATE = 1,    /* K2: x, r update, ||r||^2, AC^T y             */
+  RCG_K_UPDATE = 1,    /* K2: x, r update, ||r||^2                     */
   RCG_K_COARSE = 2,    /* coarse solve (n_c > 64)                      */
   RCG_K_PRECOND = 3,   /* K3: z = P M^-1 r, (r, z), AW^T [z w] partials */
   RCG_K_COLREDUCE = 4, /* K4: reorth partial reduction                  */
   RCG_K_WUPDATE = 5,   /* K5: w = z + beta w - W c                      */
-  RCG_K_NUM = 6
+  RCG_K_ACTR = 6,      /* K2b: AC^T (M^-1 r), projector GEMV-T (n_c > 0) */
+  RCG_K_NUM = 7
 };
 typedef struct {
   int64_t launches;

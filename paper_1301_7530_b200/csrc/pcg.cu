@@ -66,6 +66,7 @@ struct IterArgs {
   int reorth;
   int rows_per_block;      // K3 row tile
   int rows_per_block_upd;  // K2 row tile (smaller: its AC^T y GEMV-T has few columns)
+  int rows_per_block_actr; // K2b row tile (long: ~4 CTAs/SM over all column groups)
   int nb_pre;              // K3 row tiles (partial rows in part_reo / part_z)
   int nb_upd;              // K2 row tiles
   int nb_wu;               // K5 row blocks
@@ -261,12 +262,35 @@ update_kernel(const IterArgs* __restrict__ ap, int init) {
   const double* aw = a.AW.at(j);
   double* rh = a.R.base ? a.R.at(j) : nullptr;
   double rr = 0.0;
-  for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
+  // row pairs with 128-bit accesses (tiles start at multiples of 256 rows and
+  // every vector / history column is 16-B aligned), then an odd last row
+  const int64_t p0 = r0 >> 1, p1 = r1 >> 1;
+  double2* __restrict__ x2 = reinterpret_cast<double2*>(a.x);
+  double2* __restrict__ r2 = reinterpret_cast<double2*>(a.r);
+#pragma unroll 2
+  for (int64_t pi = p0 + threadIdx.x; pi < p1; pi += kThreads) {
+    double2 rv = r2[pi];
+    if (!init) {
+      if (rh) reinterpret_cast<double2*>(rh)[pi] = rv;
+      const double2 wv = reinterpret_cast<const double2*>(w)[pi];
+      const double2 av = reinterpret_cast<const double2*>(aw)[pi];
+      double2 xv = x2[pi];
+      xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, wv.x));      // x = x + alpha w
+      xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, wv.y));
+      rv.x = __dsub_rn(rv.x, __dmul_rn(alpha, av.x));      // r = r - alpha Aw
+      rv.y = __dsub_rn(rv.y, __dmul_rn(alpha, av.y));
+      x2[pi] = xv;
+      r2[pi] = rv;
+    }
+    rr += rv.x * rv.x + rv.y * rv.y;
+  }
+  if ((r1 & 1) && threadIdx.x == 0) {
+    const int64_t i = r1 - 1;
     double ri = a.r[i];
     if (!init) {
       if (rh) rh[i] = ri;
-      a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, w[i]));   // x = x + alpha w
-      ri = __dsub_rn(ri, __dmul_rn(alpha, aw[i]));          // r = r - alpha Aw
+      a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, w[i]));
+      ri = __dsub_rn(ri, __dmul_rn(alpha, aw[i]));
       a.r[i] = ri;
     }
     rr += ri * ri;
@@ -292,8 +316,8 @@ actr_kernel(const IterArgs* __restrict__ ap) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t tile = blockIdx.x, k0 = (int64_t)blockIdx.y * CG;
   const int kc = (int)min((int64_t)CG, a.n_c - k0);
-  const int64_t r0 = tile * a.rows_per_block_upd;
-  const int64_t len = min(a.n, r0 + a.rows_per_block_upd) - r0;
+  const int64_t r0 = tile * a.rows_per_block_actr;
+  const int64_t len = min(a.n, r0 + a.rows_per_block_actr) - r0;
   const int64_t pairs = len >> 1, per = (pairs + kWarps - 1) / kWarps;
   const int64_t pb = wid * per, pe = min(pairs, pb + per);
   const double* __restrict__ cols = a.AC + k0 * a.ldac + r0;
@@ -302,8 +326,16 @@ actr_kernel(const IterArgs* __restrict__ ap) {
   double acc[CG];
 #pragma unroll
   for (int c = 0; c < CG; ++c) acc[c] = 0.0;
-#pragma unroll 2
+  // all CG column loads of a row pair are issued unconditionally (a short
+  // last group re-reads its last column from L1) before any arithmetic, so
+  // each lane keeps CG + 2 LDG.128 in flight
+  const double2* __restrict__ c2 = reinterpret_cast<const double2*>(cols);
+  const int64_t ld2 = a.ldac >> 1;
+#pragma unroll 1
   for (int64_t pi = pb + lane; pi < pe; pi += 32) {
+    double2 v[CG];
+#pragma unroll
+    for (int c = 0; c < CG; ++c) v[c] = __ldcs(c2 + (c < kc ? c : kc - 1) * ld2 + pi);
     double2 y = *reinterpret_cast<const double2*>(rr + 2 * pi);
     if (inv) {
       const double2 d = *reinterpret_cast<const double2*>(inv + 2 * pi);
@@ -311,11 +343,7 @@ actr_kernel(const IterArgs* __restrict__ ap) {
       y.y = __dmul_rn(d.y, y.y);
     }
 #pragma unroll
-    for (int c = 0; c < CG; ++c)
-      if (c < kc) {
-        const double2 v = __ldcs(reinterpret_cast<const double2*>(cols + c * a.ldac) + pi);
-        acc[c] += v.x * y.x + v.y * y.y;
-      }
+    for (int c = 0; c < CG; ++c) acc[c] += v[c].x * y.x + v[c].y * y.y;
   }
   if ((len & 1) && wid == kWarps - 1 && lane == 0) {
     const int64_t i = len - 1;
@@ -912,6 +940,19 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   static const int upd_tiles = env_int("RCG_UPD_TILES_PER_SM", 4);
   const int Ru = n_c ? rows_per_block_for(c, n, upd_tiles) : big_tile(rows_per_block_for(c, n, upd_tiles));
   const int nbu = (int)std::max<int64_t>(1, ceil_div(n, Ru));
+  // K2b: exactly one wave of resident CTAs over all (tile, 8-column group)
+  // pairs (a 1.3-wave grid ran its tail at a third of the SMs: 3.4 TB/s), so
+  // each warp streams long runs (at most nbu tiles: the partial rows are K2's)
+  static const int actr_occ = [] {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, actr_kernel, kThreads, 0) != cudaSuccess || occ < 1)
+      occ = 2;
+    return occ * env_int("RCG_ACTR_WAVES", 1);
+  }();
+  const int64_t ngr = std::max<int64_t>(1, ceil_div(n_c, 8));
+  const int64_t nta0 = std::max<int64_t>(1, std::min<int64_t>(nbu, (int64_t)actr_occ * c->num_sms / ngr));
+  const int Ra = (int)(ceil_div(ceil_div(n, nta0), (int64_t)2) * 2);
+  const int nta = (int)std::max<int64_t>(1, ceil_div(n, Ra));
   const int nbs = spmv_partials(c, A);
   // K3 column splits for small n (the AW GEMV-T otherwise runs on nb CTAs only)
   const int pre_split = reorth ? (int)std::max<int64_t>(1, std::min<int64_t>(8, (2 * c->num_sms) / nb)) : 1;
@@ -1050,6 +1091,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     a.reorth = reorth ? 1 : 0;
     a.rows_per_block = R;
     a.rows_per_block_upd = Ru;
+    a.rows_per_block_actr = Ra;
     a.nb_pre = nb;
     a.nb_upd = nbu;
     a.nb_wu = wu_grid;
@@ -1161,7 +1203,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   update_kernel<<<nbu_l, kThreads, 0, c->stream>>>(dargs, 1);
   RCG_LAUNCH_CHECK(c);
   if (n_c) {
-    actr_kernel<<<dim3(nbu, (unsigned)ceil_div(n_c, 8)), kThreads, 0, c->stream>>>(dargs);
+    actr_kernel<<<dim3(nta, (unsigned)ngr), kThreads, 0, c->stream>>>(dargs);
     RCG_LAUNCH_CHECK(c);
   }
   if ((rc = allreduce_h(H, c, gSum.ptr + 1, (size_t)(1 + n_c)))) return fail(rc);
@@ -1205,14 +1247,16 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
       if ((rc2 = launch_spmv_ind(c, A, &dargs->spmv))) return rc2;
       if (direct) prof_end(c);
       if ((rc2 = allreduce_h(H, c, gSum.ptr, 1))) return rc2;
-      if (direct) prof_begin(c, RCG_K_UPDATE, 8.0 * nd * (6 + jac + n_c + (store ? 1 : 0)));
+      if (direct) prof_begin(c, RCG_K_UPDATE, 8.0 * nd * (6 + (store ? 1 : 0)));
       update_kernel<<<nbu_l, kThreads, 0, c->stream>>>(dargs, 0);
       RCG_LAUNCH_CHECK(c);
-      if (n_c) {
-        actr_kernel<<<dim3(nbu, (unsigned)ceil_div(n_c, 8)), kThreads, 0, c->stream>>>(dargs);
-        RCG_LAUNCH_CHECK(c);
-      }
       if (direct) prof_end(c);
+      if (n_c) {
+        if (direct) prof_begin(c, RCG_K_ACTR, 8.0 * nd * (1 + jac + n_c));
+        actr_kernel<<<dim3(nta, (unsigned)ngr), kThreads, 0, c->stream>>>(dargs);
+        RCG_LAUNCH_CHECK(c);
+        if (direct) prof_end(c);
+      }
       if ((rc2 = allreduce_h(H, c, gSum.ptr + 1, (size_t)(1 + n_c)))) return rc2;
       if (n_c > NC_INLINE) {
         if (direct) prof_begin(c, RCG_K_COARSE, 8.0 * (double)n_c * (double)n_c);
@@ -1275,7 +1319,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
       char key[256];
       snprintf(key, sizeof(key), "%p|%lld|%d|%d|%d|%d|%zu|%zu|%d|%d|%lld|%d|%d", (void*)pre, (long long)n,
                spmv_width(A), nbs, nb, nbu, smem_upd, smem_pre, reorth ? 1 : 0, n_c > NC_INLINE ? 1 : 0,
-               (long long)B, A->block, A->row_offsets_64 + 2 * (int)ceil_div(n_c, 8));
+               (long long)B, A->block + 100 * A->bsr_slice, A->row_offsets_64 + 2 * (int)ceil_div(n_c, 8));
       cudaGraphExec_t exec = nullptr;
       auto gi = c->graphs.find(key);
       if (gi != c->graphs.end()) {
