@@ -401,8 +401,10 @@ coarse_kernel(const IterArgs* __restrict__ ap, int check_done) {
 // ---------------------------------------------------------------------------
 // K3: convergence test, z = M^{-1} r - C s, (r, z), reorth partials
 
-template <int CG, bool PF>
-__global__ void __launch_bounds__(kThreads, 2)
+// REO = false: the lean no-reorth variant (no GEMV code, so no 128-register
+// budget): 4 CTAs/SM keep enough row loads in flight for the z pass
+template <int CG, bool PF, bool REO>
+__global__ void __launch_bounds__(kThreads, REO ? 2 : 4)
 precond_kernel(const IterArgs* __restrict__ ap, int init) {
   const IterArgs& a = *ap;
   SolveState* st = a.st;
@@ -447,33 +449,56 @@ precond_kernel(const IterArgs* __restrict__ ap, int init) {
   double* z = init ? a.Z.at(j) : a.Z.at(j + 1);
   double* w0 = init ? a.W.at(j) : nullptr;
   const double* wj = a.W.at(j);
-  const bool reo = a.reorth && !init;
+  const bool reo = REO && a.reorth && !init;
   // column splits (small n): split 0 owns the z / (r, z) outputs, every split
   // rebuilds the z tile and streams its share of the AW columns
   const int split = blockIdx.y, S = gridDim.y;
   const bool lead = split == 0;
   double rz = 0.0;
-  for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
-    const double ri = a.r[i];
-    double zi = a.inv_diag ? __dmul_rn(a.inv_diag[i], ri) : ri;
-    if (a.n_c) {
-      double cs = 0.0;
-      for (int64_t c = 0; c < a.n_c; ++c) cs += a.C[c * a.ldc + i] * s[c];
-      zi = __dsub_rn(zi, cs);                               // y - C s  (solver.py:91)
+  // ZB rows per thread per step, every load of the step issued before the
+  // step's stores (z may alias r / W for the compiler, which would otherwise
+  // serialize one HBM round trip per row); rows i, i + 256, ... keep the
+  // per-thread (r, z) summation order of a plain row loop
+  constexpr int ZB = 4;
+  for (int64_t ib = r0 + threadIdx.x; ib < r1; ib += ZB * kThreads) {
+    double rv[ZB], zv[ZB], wv[ZB];
+#pragma unroll
+    for (int u = 0; u < ZB; ++u) {
+      const int64_t i = ib + u * kThreads;
+      rv[u] = i < r1 ? a.r[i] : 0.0;
+      zv[u] = (i < r1 && a.inv_diag) ? a.inv_diag[i] : 1.0;
+      wv[u] = (reo && i < r1) ? wj[i] : 0.0;
     }
-    if (lead) {
-      z[i] = zi;
-      if (w0) w0[i] = zi;                                   // w_0 = z_0 (solver.py:231)
+#pragma unroll
+    for (int u = 0; u < ZB; ++u) {
+      const int64_t i = ib + u * kThreads;
+      double zi = a.inv_diag ? __dmul_rn(zv[u], rv[u]) : rv[u];
+      if (a.n_c && i < r1) {
+        double cs = 0.0;
+        for (int64_t c = 0; c < a.n_c; ++c) cs += a.C[c * a.ldc + i] * s[c];
+        zi = __dsub_rn(zi, cs);                             // y - C s  (solver.py:91)
+      }
+      zv[u] = zi;
     }
-    rz += ri * zi;
-    if (reo) {
-      ztile[i - r0] = zi;
-      wtile[i - r0] = wj[i];
+#pragma unroll
+    for (int u = 0; u < ZB; ++u) {
+      const int64_t i = ib + u * kThreads;
+      if (i >= r1) break;
+      const double zi = zv[u];
+      if (lead) {
+        z[i] = zi;
+        if (w0) w0[i] = zi;                                 // w_0 = z_0 (solver.py:231)
+      }
+      rz += rv[u] * zi;
+      if (reo) {
+        ztile[i - r0] = zi;
+        wtile[i - r0] = wv[u];
+      }
     }
   }
   const double rzb = block_sum<kThreads>(rz, sm);
   if (lead && threadIdx.x == 0) a.part_z[blockIdx.x] = rzb;
-  if (reo) {
+  if (REO && reo) {
     __syncthreads();
     // AW is fully stored when reorthogonalizing (mod 0): column k at base + k*ld
     __shared__ double red[kWarps * CG * 2];
@@ -515,7 +540,9 @@ colreduce_kernel(const IterArgs* __restrict__ ap) {
 // ---------------------------------------------------------------------------
 // K5: beta, w_{j+1} = z + beta w_j  (- W c' with c' = (AW^T w)/diag)
 
-template <int RPT>
+// BATCH (no reorth): the finisher issues all its loads before any store;
+// with reorth the interleaved finisher keeps the W GEMV's registers
+template <int RPT, bool BATCH>
 __global__ void __launch_bounds__(kThreads)
 wupdate_kernel(const IterArgs* __restrict__ ap) {
   const IterArgs& a = *ap;
@@ -608,7 +635,7 @@ wupdate_kernel(const IterArgs* __restrict__ ap) {
       }
     }
   }
-  if (finisher) {
+  if (finisher && !BATCH) {
     const double* z = a.Z.at(j + 1);
     const double* wo = a.W.at(j);
     double* wn = a.W.at(j + 1);
@@ -617,6 +644,29 @@ wupdate_kernel(const IterArgs* __restrict__ ap) {
       const int64_t i = r0 + threadIdx.x + q * kThreads;
       if (i < a.n) {
         double v = __dadd_rn(z[i], __dmul_rn(beta, wo[i]));   // w = z + beta w
+        if (a.reorth) v = __dsub_rn(v, acc[q]);                // w -= W c'
+        wn[i] = v;
+      }
+    }
+  }
+  if (finisher && BATCH) {
+    const double* z = a.Z.at(j + 1);
+    const double* wo = a.W.at(j);
+    double* wn = a.W.at(j + 1);
+    // all 2 x RPT loads before the first store (wn may alias z / wo for the
+    // compiler: interleaved, every row would cost one HBM round trip)
+    double zq[RPT], wq[RPT];
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int64_t i = r0 + threadIdx.x + q * kThreads;
+      zq[q] = i < a.n ? z[i] : 0.0;
+      wq[q] = i < a.n ? wo[i] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int64_t i = r0 + threadIdx.x + q * kThreads;
+      if (i < a.n) {
+        double v = __dadd_rn(zq[q], __dmul_rn(beta, wq[q]));  // w = z + beta w
         if (a.reorth) v = __dsub_rn(v, acc[q]);                // w -= W c'
         wn[i] = v;
       }
@@ -1118,9 +1168,10 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
                                    (int)std::max<size_t>(smem_upd, 1024)));
   static const int pre_cg = env_int("RCG_PRE_CG", 8);
   static const bool pre_pf = env_int("RCG_PF", 1) != 0;
-  auto pre = pre_cg == 4 ? precond_kernel<4, false>
-                         : (pre_cg == 2 ? precond_kernel<2, false>
-                                        : (pre_pf ? precond_kernel<8, true> : precond_kernel<8, false>));
+  auto pre = !reorth ? precond_kernel<8, false, false>
+             : (pre_cg == 4 ? precond_kernel<4, false, true>
+                            : (pre_cg == 2 ? precond_kernel<2, false, true>
+                                           : (pre_pf ? precond_kernel<8, true, true> : precond_kernel<8, false, true>)));
   RCG_CUDA(c, cudaFuncSetAttribute(pre, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(smem_pre, 1024)));
 
@@ -1276,12 +1327,16 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
       // one packed allreduce: (r, z) and the 2(j+1) reorth dot products
       if ((rc2 = allreduce_h(H, c, gSum.ptr + a.rz_off, (size_t)(1 + (reorth ? 2 * (jj + 1) : 0))))) return rc2;
       if (direct) prof_begin(c, RCG_K_WUPDATE, 8.0 * nd * (3 + (reorth ? js : 0.0)));
-      if (wu_rpt == 16)
-        wupdate_kernel<16><<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
-      else if (wu_rpt == 8)
-        wupdate_kernel<8><<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
-      else
-        wupdate_kernel<WU_RPT><<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
+      if (!reorth) {
+        if (wu_rpt == 16)
+          wupdate_kernel<16, true><<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
+        else
+          wupdate_kernel<WU_RPT, true><<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
+      } else if (wu_rpt == 8) {
+        wupdate_kernel<8, false><<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
+      } else {
+        wupdate_kernel<WU_RPT, false><<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
+      }
       RCG_LAUNCH_CHECK(c);
       if (direct) prof_end(c);
     }
