@@ -69,7 +69,14 @@ typedef struct {
                                        [ceil(n/96)+1] chunk slot offsets,
                                        bsr_col_indices [32*slots] (-1 = pad),
                                        bsr_values [288*slots] */
-  int32_t pad0;
+  int32_t dia_count;                /* > 0: symmetric block-diagonal (DIA) copy */
+  int32_t dia_block;                /* DIA unit: 1 (scalar) or 3 (3x3 blocks)  */
+  int32_t pad1;
+  const int64_t* dia_offsets;       /* [dia_count] upper block-diagonal offsets,
+                                       ascending, dia_offsets[0] = 0 (device) */
+  const double* dia_values;         /* [dia_count][b*b][n/b]: entry (i, jj) of
+                                       block (p, p + off_d) at
+                                       ((d*b + i)*b + jj)*(n/b) + p; 0 = absent */
 } rcg_csr;
 
 /* Deflation operator P = I - C G^{-1} (AC)^T, G = C^T A C (DeflationOperator,
@@ -231,6 +238,19 @@ int rcg_gen_diffusion_fill(rcg_ctx* ctx, const int64_t* dims, int32_t ndim, cons
 int rcg_gen_elasticity_rows(rcg_ctx* ctx, int64_t nelem, int64_t* ro64, int64_t* nnz_host);
 int rcg_gen_elasticity_fill(rcg_ctx* ctx, int64_t nelem, const double* Ke, const double* E,
                             const int64_t* ro64, int32_t* ro32, int32_t* ci, double* va);
+/* Symmetric block-diagonal (DIA) copy for grid operators whose entries lie on
+ * a few block diagonals (5/7-point stencils with b = 1, Q1 elasticity with
+ * b = 3): only the upper diagonals are stored, A(p, p - o) = A(p - o, p)^T
+ * is read from the row p - o (both streams coalesced, no column indices).
+ * analyze: the distinct block offsets of the longest row, verified against
+ * every entry; *nd_host = their count (0: not DIA-structured; at most 64),
+ * offs_host[0..nd) ascending (synchronizes).
+ * build: offs = the upper offsets (>= 0, ascending, device), nd_up of them;
+ * fills U[nd_up][b*b][n/b] and checks exact symmetry (values and pattern):
+ * *symmetric_host = 1 when the copy reproduces A, else 0 (do not use it). */
+int rcg_csr_dia_analyze(rcg_ctx* ctx, const rcg_csr* A, int32_t b, int64_t* offs_host, int32_t* nd_host);
+int rcg_csr_dia_build(rcg_ctx* ctx, const rcg_csr* A, int32_t b, const int64_t* offs, int32_t nd_up, double* U,
+                      int32_t* symmetric_host);
 /* elementwise y = inv_diag * x (Preconditioner.apply, solver.py:50-54) */
 int rcg_diag_apply(rcg_ctx* ctx, int64_t n, const double* inv_diag, const double* x, double* y);
 

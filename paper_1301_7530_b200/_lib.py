@@ -30,7 +30,8 @@ class RcgCsr(C.Structure):
                 ("row_offsets_64", C.c_int32), ("block", C.c_int32),
                 ("col_indices", C.c_void_p), ("values", C.c_void_p),
                 ("bsr_row_offsets", C.c_void_p), ("bsr_col_indices", C.c_void_p), ("bsr_values", C.c_void_p),
-                ("bsr_slice", C.c_int32), ("pad0", C.c_int32)]
+                ("bsr_slice", C.c_int32), ("dia_count", C.c_int32), ("dia_block", C.c_int32), ("pad1", C.c_int32),
+                ("dia_offsets", C.c_void_p), ("dia_values", C.c_void_p)]
 
 
 class RcgDeflation(C.Structure):
@@ -100,6 +101,8 @@ SIGNATURES = {
     "rcg_gen_diffusion_fill": (C.c_int, [_vp, _vp, C.c_int32, _vp, _vp, _vp, _vp, _vp]),
     "rcg_gen_elasticity_rows": (C.c_int, [_vp, C.c_int64, _vp, C.POINTER(C.c_int64)]),
     "rcg_gen_elasticity_fill": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "rcg_csr_dia_analyze": (C.c_int, [_vp, C.POINTER(RcgCsr), C.c_int32, _vp, C.POINTER(C.c_int32)]),
+    "rcg_csr_dia_build": (C.c_int, [_vp, C.POINTER(RcgCsr), C.c_int32, _vp, C.c_int32, _vp, C.POINTER(C.c_int32)]),
     "rcg_csr_block3_slice_plan": (C.c_int, [_vp, C.POINTER(RcgCsr), _vp, C.POINTER(C.c_int64)]),
     "rcg_csr_block3_slice_build": (C.c_int, [_vp, C.POINTER(RcgCsr), _vp, _vp, _vp]),
     "rcg_diag_apply": (C.c_int, [_vp, _i64, _vp, _vp, _vp]),

@@ -77,13 +77,42 @@ def colmajor_from_host(M, ld=None):
 
 
 class _DevCsr:
-    __slots__ = ("ro", "ci", "va", "bro", "bci", "bval", "struct")
+    __slots__ = ("ro", "ci", "va", "bro", "bci", "bval", "doffs", "dvals", "struct")
 
     def __init__(self, ro, ci, va, n, nnz, ro64):
         self.ro, self.ci, self.va = ro, ci, va
         self.bro = self.bci = self.bval = None
+        self.doffs = self.dvals = None
         self.struct = _lib.RcgCsr(n, nnz, ro.data_ptr(), 1 if ro64 else 0, 0, ci.data_ptr(), va.data_ptr(),
                                   None, None, None)
+
+    def add_dia(self, ctx, b):
+        """Attach a symmetric block-DIA copy (spmv.cu ``dia_body``) when every
+        entry lies on a few block diagonals, the operator is exactly
+        symmetric and the stored upper blocks stream fewer bytes than CSR.
+        Returns False (nothing attached) otherwise."""
+        torch = _torch()
+        n, nnz = int(self.struct.n), int(self.struct.nnz)
+        offs = (_lib.C.c_int64 * 64)()
+        nd = _lib.C.c_int32(0)
+        ctx.check(ctx.lib.rcg_csr_dia_analyze(ctx.h, _lib.C.byref(self.struct), b, offs, _lib.C.byref(nd)),
+                  "dia_analyze")
+        up = [offs[i] for i in range(nd.value) if offs[i] >= 0]
+        if not up or 8.0 * len(up) * b * n > 8.0 * nnz + 4.0 * nnz / (9 if b == 3 else 1):
+            return False
+        doffs = torch.tensor(up, dtype=torch.int64, device="cuda")
+        dvals = torch.empty(len(up) * b * n, dtype=torch.float64, device="cuda")
+        sym = _lib.C.c_int32(0)
+        ctx.check(ctx.lib.rcg_csr_dia_build(ctx.h, _lib.C.byref(self.struct), b, _lib.ptr(doffs), len(up),
+                                            _lib.ptr(dvals), _lib.C.byref(sym)), "dia_build")
+        if not sym.value:
+            return False
+        self.doffs, self.dvals = doffs, dvals
+        self.struct.dia_offsets = doffs.data_ptr()
+        self.struct.dia_values = dvals.data_ptr()
+        self.struct.dia_block = b
+        self.struct.dia_count = len(up)
+        return True
 
     def add_block3(self, ctx):
         """Detect 3x3 block structure on the device and attach a BSR copy
@@ -282,7 +311,16 @@ class SparseSpdMatrix:
 
 
 def _maybe_block3(h, n, nnz, use_block3):
-    if use_block3 and _os.environ.get("RCG_BSR", "1") != "0" and n % 3 == 0 and nnz % 9 == 0 and nnz >= 9 * n // 3 * 2:
+    """Pick the SpMV stream format: symmetric block-DIA for grid operators
+    (stencils, structured Q1 meshes), else sliced 3x3 blocks for
+    block-structured FEM operators, else scalar CSR."""
+    if not use_block3:
+        return
+    blocky = n % 3 == 0 and nnz % 9 == 0 and nnz >= 9 * n // 3 * 2
+    if _os.environ.get("RCG_DIA", "1") != "0" and n > 0:
+        if h.add_dia(_lib.context(), 3 if blocky else 1):
+            return
+    if _os.environ.get("RCG_BSR", "1") != "0" and blocky:
         h.add_block3(_lib.context())
 
 

@@ -1277,7 +1277,9 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   const double jac = inv_diag ? 1.0 : 0.0;
   // algorithmic bytes of the format actually streamed (BSR3: one index per block)
   const double bytes_spmv =
-      (A->block == 3 && A->bsr_row_offsets)
+      A->dia_count > 0
+          ? 8.0 * A->dia_count * A->dia_block * (double)n + 16.0 * (double)n   // stored upper blocks + x, y
+      : (A->block == 3 && A->bsr_row_offsets)
           ? 8.0 * (double)A->nnz + 4.0 * (double)A->nnz / 9.0 + 4.0 * (double)(n / 3 + 1) + 16.0 * (double)n
           : 12.0 * (double)A->nnz + (A->row_offsets_64 ? 8.0 : 4.0) * (double)(n + 1) + 16.0 * (double)n;
   static const int use_graphs = env_int("RCG_GRAPHS", 1);
@@ -1374,7 +1376,8 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
       char key[256];
       snprintf(key, sizeof(key), "%p|%lld|%d|%d|%d|%d|%zu|%zu|%d|%d|%lld|%d|%d", (void*)pre, (long long)n,
                spmv_width(A), nbs, nb, nbu, smem_upd, smem_pre, reorth ? 1 : 0, n_c > NC_INLINE ? 1 : 0,
-               (long long)B, A->block + 100 * A->bsr_slice, A->row_offsets_64 + 2 * (int)ceil_div(n_c, 8));
+               (long long)B, A->block + 100 * A->bsr_slice + 10000 * (A->dia_count * 4 + A->dia_block),
+               A->row_offsets_64 + 2 * (int)ceil_div(n_c, 8));
       cudaGraphExec_t exec = nullptr;
       auto gi = c->graphs.find(key);
       if (gi != c->graphs.end()) {

@@ -18,6 +18,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <vector>
+#include <map>
+#include <mutex>
 
 #ifndef RCG_SPMV_MINB
 #define RCG_SPMV_MINB 4
@@ -353,6 +355,251 @@ int sell3_grid(Ctx* c, int64_t nbr) {
   return (int)std::max<int64_t>(1, std::min(g, cap));
 }
 
+// ---------------------------------------------------------------------------
+// Symmetric block-DIA SpMV (b = 1: 5/7-point stencils; b = 3: Q1 elasticity
+// on a structured grid).  Thread per block row p.  Only the nd upper block
+// diagonals are stored (U_d(p) = A(p, p + o_d), o_0 = 0); the lower blocks
+// are the transposes A(p, p - o) = U_d(p - o)^T.  Every load is a coalesced
+// stream (values at p and at p - o, x at b(p +- o)), no column indices are
+// read, and each stored block feeds two rows: 8 b^2 nd bytes per block row
+// instead of 12 bytes per stored entry.  Row sums accumulate entry by entry
+// in ascending column order (the CSR order).
+
+constexpr int DIA_MAX = 64;
+
+// ND > 0: the diagonal count is a compile-time constant (5/7-point: 3/4
+// upper diagonals, Q1 27-point blocks: 14), so both diagonal loops unroll
+// fully and every value / x load of a row is independent and in flight at
+// once; ND = 0 is the generic runtime-count loop.
+template <int B, int MODE, int ND>
+__device__ __forceinline__ bool dia_body(int64_t nbr, int nd_rt, const int64_t* __restrict__ offs /* smem */,
+                                         const double* __restrict__ U, const ColSel& xs, const ColSel& ys,
+                                         const double* __restrict__ b, const SolveState* st, double& d0, double& d1) {
+  long long j = 0;
+  if (st) {
+    if (st->done) return false;
+    j = st->j;
+  }
+  const double* __restrict__ x = xs.at(j);
+  double* __restrict__ y = ys.at(j);
+  constexpr int BB = B * B;
+  const int nd = ND > 0 ? ND : nd_rt;
+  d0 = 0.0;
+  d1 = 0.0;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nbr; p += (int64_t)gridDim.x * blockDim.x) {
+    double acc[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) acc[i] = 0.0;
+    // Terms t = 0 .. 2nd-2 in ascending block-column order: t < nd-1 is the
+    // lower block d = nd-1-t (transposed U_d(p - o)), then the diagonal and
+    // upper blocks d = t-(nd-1).  Branch-free: an out-of-range block loads
+    // from a clamped valid address and adds fma(0, 0, acc).  K terms per
+    // step load everything before the first FMA (in-order issue would
+    // otherwise stall each step's loads behind the previous step's FMAs).
+    constexpr int K = B == 1 ? 8 : 2;
+    const int nt = 2 * nd - 1;
+    double xd[B];   // x of this block row (the o = 0 block), kept for the (x, y) dot
+#pragma unroll(ND > 0 ? (2 * ND - 1 + K - 1) / K : 1)
+    for (int t0 = 0; t0 < nt; t0 += K) {
+      double v[K][BB], xv[K][B];
+      bool ok[K], lower[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int t = t0 + k;
+        lower[k] = t < nd - 1;
+        const int d = t >= nt ? 0 : (lower[k] ? nd - 1 - t : t - (nd - 1));
+        const int64_t o = offs[d];
+        ok[k] = t < nt && (lower[k] ? p >= o : p + o < nbr);
+        const int64_t ub = lower[k] ? (ok[k] ? p - o : 0) : p;        // block row of the stored U_d
+        const int64_t xb = lower[k] ? ub : (ok[k] ? p + o : p);       // block column
+#pragma unroll
+        for (int jj = 0; jj < B; ++jj) xv[k][jj] = __ldg(x + B * xb + jj);
+        const double* __restrict__ u = U + (int64_t)d * BB * nbr + ub;
+#pragma unroll
+        for (int q = 0; q < BB; ++q) v[k][q] = __ldg(u + (int64_t)q * nbr);
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (t0 + k == nd - 1) {
+#pragma unroll
+          for (int jj = 0; jj < B; ++jj) xd[jj] = xv[k][jj];
+        }
+#pragma unroll
+        for (int i = 0; i < B; ++i)
+#pragma unroll
+          for (int jj = 0; jj < B; ++jj) {
+            const double a = lower[k] ? v[k][jj * B + i] : v[k][i * B + jj];
+            acc[i] = fma(ok[k] ? a : 0.0, ok[k] ? xv[k][jj] : 0.0, acc[i]);
+          }
+      }
+    }
+    const int64_t r = B * p;
+    double bv[B];
+    if (MODE == 2) {
+#pragma unroll
+      for (int i = 0; i < B; ++i) bv[i] = b[r + i];
+    }
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      double a = acc[i];
+      if (MODE == 2) {
+        a = bv[i] - a;
+        d1 += bv[i] * bv[i];
+        d0 += a * a;
+      } else if (MODE == 1) {
+        d0 += xd[i] * a;
+      }
+      acc[i] = a;
+    }
+#pragma unroll
+    for (int i = 0; i < B; ++i) y[r + i] = acc[i];   // no load of this row after its stores
+  }
+  return true;
+}
+
+__device__ __forceinline__ void dia_load_offsets(int nd, const int64_t* __restrict__ g, int64_t* sm) {
+  for (int d = threadIdx.x; d < nd; d += blockDim.x) sm[d] = g[d];
+  __syncthreads();
+}
+
+template <int B, int MODE, int ND>
+__global__ void __launch_bounds__(kThreads)
+dia_kernel(int64_t nbr, int nd, const int64_t* __restrict__ offs, const double* __restrict__ U, ColSel xs, ColSel ys,
+           const double* __restrict__ b, const SolveState* st, double* part, unsigned int* counter, double* out) {
+  __shared__ int64_t so[DIA_MAX];
+  dia_load_offsets(nd, offs, so);
+  double d0, d1;
+  if (dia_body<B, MODE, ND>(nbr, nd, so, U, xs, ys, b, st, d0, d1)) spmv_epilogue<MODE>(d0, d1, part, counter, out);
+}
+
+template <int B, int ND>
+__global__ void __launch_bounds__(kThreads) dia_kernel_ind(const SpmvArgs* __restrict__ sa) {
+  __shared__ int64_t so[DIA_MAX];
+  const int nd = sa->dia_nd;
+  dia_load_offsets(nd, sa->dia_offsets, so);
+  double d0, d1;
+  if (dia_body<B, 1, ND>(sa->n / B, nd, so, sa->dia_values, sa->xs, sa->ys, nullptr, sa->st, d0, d1))
+    spmv_epilogue<1>(d0, d1, sa->part, sa->counter, sa->out);
+}
+
+// Exactly one wave of resident CTAs of the kernel actually launched (its own
+// occupancy: the variants use 32-100 registers): a grid-stride sweep then
+// moves through the rows as one front, so the lower blocks U_d(p - o) and the
+// x entries at p - o are still in L2 when row p reads them (a second wave
+// re-reads them from HBM: +19% bytes and 2x the time at 256^3).
+int occupancy_of(const void* kernel) {
+  static std::mutex mu;
+  static std::map<const void*, int> cache;
+  std::lock_guard<std::mutex> l(mu);
+  auto it = cache.find(kernel);
+  if (it != cache.end()) return it->second;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, 0) != cudaSuccess || occ < 1) occ = 1;
+  return cache[kernel] = occ;
+}
+
+int dia_grid(Ctx* c, int64_t nbr, const void* kernel) {
+  static const int forced = [] {
+    const char* e = getenv("RCG_DIA_CTAS");
+    return e ? std::max(1, atoi(e)) : 0;
+  }();
+  const int64_t g = ceil_div(nbr, kThreads);
+  const int64_t cap = (int64_t)c->num_sms * (forced ? forced : occupancy_of(kernel));
+  return (int)std::max<int64_t>(1, std::min(g, cap));
+}
+
+// longest row (ties: lowest index) as (len << 32) | (0xffffffff - row) for atomicMax
+template <typename RO>
+__global__ void longest_row_kernel(int64_t n, const RO* __restrict__ ro, unsigned long long* best) {
+  unsigned long long m = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long len = (unsigned long long)(ro[i + 1] - ro[i]);
+    const unsigned long long key = (len << 32) | (0xffffffffull - (unsigned long long)i);
+    m = key > m ? key : m;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t = __shfl_xor_sync(0xffffffffu, m, o);
+    m = t > m ? t : m;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(best, m);
+}
+
+__device__ __forceinline__ int dia_find(const int64_t* so, int nd, int64_t o) {
+  int lo = 0, hi = nd - 1;
+  while (lo <= hi) {
+    const int mid = (lo + hi) >> 1;
+    if (so[mid] == o) return mid;
+    if (so[mid] < o) lo = mid + 1;
+    else hi = mid - 1;
+  }
+  return -1;
+}
+
+// every entry's block offset must be one of the nd candidates
+template <typename RO>
+__global__ void dia_verify_kernel(int64_t n, int B, const RO* __restrict__ ro, const int32_t* __restrict__ ci,
+                                  const int64_t* __restrict__ offs, int nd, int* bad) {
+  __shared__ int64_t so[DIA_MAX];
+  dia_load_offsets(nd, offs, so);
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pr = r / B;
+    for (int64_t k = ro[r]; k < ro[r + 1]; ++k)
+      if (ci[k] >= n || dia_find(so, nd, (int64_t)ci[k] / B - pr) < 0) {   // ghost columns: not a DIA operator
+        atomicExch(bad, 1);
+        return;
+      }
+  }
+}
+
+// scatter the diagonal and upper blocks into U (diagonal blocks whole);
+// count strictly-lower / strictly-upper entries
+template <typename RO>
+__global__ void dia_fill_kernel(int64_t n, int B, const RO* __restrict__ ro, const int32_t* __restrict__ ci,
+                                const double* __restrict__ va, const int64_t* __restrict__ offs, int nd, double* U,
+                                unsigned long long* counts) {
+  __shared__ int64_t so[DIA_MAX];
+  dia_load_offsets(nd, offs, so);
+  const int64_t nbr = n / B;
+  unsigned long long lo = 0, up = 0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pr = r / B, i = r % B;
+    for (int64_t k = ro[r]; k < ro[r + 1]; ++k) {
+      const int64_t c = ci[k];
+      if (c < r) ++lo;
+      if (c > r) ++up;
+      if (c / B < pr) continue;   // strictly lower block: read from the transpose
+      const int d = dia_find(so, nd, c / B - pr);
+      U[((int64_t)(d * B + i) * B + c % B) * nbr + pr] = va[k];
+    }
+  }
+  atomicAdd(counts, lo);
+  atomicAdd(counts + 1, up);
+}
+
+// every strictly-lower entry equals its stored transpose (bitwise)
+template <typename RO>
+__global__ void dia_sym_kernel(int64_t n, int B, const RO* __restrict__ ro, const int32_t* __restrict__ ci,
+                               const double* __restrict__ va, const int64_t* __restrict__ offs, int nd,
+                               const double* __restrict__ U, int* bad) {
+  __shared__ int64_t so[DIA_MAX];
+  dia_load_offsets(nd, offs, so);
+  const int64_t nbr = n / B;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pr = r / B, i = r % B;
+    for (int64_t k = ro[r]; k < ro[r + 1]; ++k) {
+      const int64_t c = ci[k];
+      if (c >= r) continue;
+      const int64_t pc = c / B, jj = c % B;
+      const int d = dia_find(so, nd, pr - pc);   // A(r, c) = A(c, r) = U_d(pc)[jj][i]
+      if (d < 0 ||
+          __double_as_longlong(U[((int64_t)(d * B + jj) * B + i) * nbr + pc]) != __double_as_longlong(va[k])) {
+        atomicExch(bad, 1);
+        return;
+      }
+    }
+  }
+}
+
 // chunk widths (max blocks per block row over each 32-row chunk) from plain BSR
 __global__ void sell3_width_kernel(int64_t nbr, const int32_t* __restrict__ bro, int32_t* widths) {
   const int64_t nchunks = (nbr + 31) >> 5;
@@ -588,12 +835,61 @@ static void launch_v(int V, int grid, cudaStream_t s, const rcg_csr* A, ColSel x
 #undef RCG_SPMV_CASE
 }
 
+static inline bool is_dia(const rcg_csr* A) {
+  return A->dia_count > 0 && A->dia_values && (A->dia_block == 1 || A->dia_block == 3);
+}
 static inline bool is_sell3(const rcg_csr* A) {
   return A->block == 3 && A->bsr_slice == 32 && A->bsr_row_offsets;
 }
 
+template <int B, int ND>
+static void launch_dia_nd(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const double* b,
+                          const SolveState* st, double* part, unsigned int* counter, double* out) {
+  const int64_t nbr = A->n / B;
+  auto k = mode == 0 ? dia_kernel<B, 0, ND> : (mode == 1 ? dia_kernel<B, 1, ND> : dia_kernel<B, 2, ND>);
+  k<<<dia_grid(c, nbr, (const void*)k), kThreads, 0, c->stream>>>(nbr, A->dia_count, A->dia_offsets, A->dia_values,
+                                                                  xs, ys, b, st, part, counter, out);
+}
+
+// grid (= partial-sum slots) of the DIA kernel that launch_spmv{,_ind} would use
+static int dia_grid_for(Ctx* c, const rcg_csr* A, int mode, bool ind) {
+  const int64_t nbr = A->n / A->dia_block;
+  const int nd = A->dia_count;
+  const void* k;
+  if (A->dia_block == 3) {
+    if (ind) k = nd == 14 ? (const void*)dia_kernel_ind<3, 14> : (const void*)dia_kernel_ind<3, 0>;
+    else if (nd == 14) k = mode == 0 ? (const void*)dia_kernel<3, 0, 14> : mode == 1 ? (const void*)dia_kernel<3, 1, 14> : (const void*)dia_kernel<3, 2, 14>;
+    else k = mode == 0 ? (const void*)dia_kernel<3, 0, 0> : mode == 1 ? (const void*)dia_kernel<3, 1, 0> : (const void*)dia_kernel<3, 2, 0>;
+  } else {
+    if (ind) k = nd == 3 ? (const void*)dia_kernel_ind<1, 3> : nd == 4 ? (const void*)dia_kernel_ind<1, 4> : (const void*)dia_kernel_ind<1, 0>;
+    else if (nd == 3) k = mode == 0 ? (const void*)dia_kernel<1, 0, 3> : mode == 1 ? (const void*)dia_kernel<1, 1, 3> : (const void*)dia_kernel<1, 2, 3>;
+    else if (nd == 4) k = mode == 0 ? (const void*)dia_kernel<1, 0, 4> : mode == 1 ? (const void*)dia_kernel<1, 1, 4> : (const void*)dia_kernel<1, 2, 4>;
+    else k = mode == 0 ? (const void*)dia_kernel<1, 0, 0> : mode == 1 ? (const void*)dia_kernel<1, 1, 0> : (const void*)dia_kernel<1, 2, 0>;
+  }
+  return dia_grid(c, nbr, k);
+}
+
+// compile-time diagonal counts: 5-point (3), 7-point (4), Q1 27-point blocks (14)
+static void launch_dia(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const double* b,
+                       const SolveState* st, double* part, unsigned int* counter, double* out) {
+  const int nd = A->dia_count;
+  if (A->dia_block == 3) {
+    if (nd == 14) launch_dia_nd<3, 14>(c, A, mode, xs, ys, b, st, part, counter, out);
+    else launch_dia_nd<3, 0>(c, A, mode, xs, ys, b, st, part, counter, out);
+  } else {
+    if (nd == 3) launch_dia_nd<1, 3>(c, A, mode, xs, ys, b, st, part, counter, out);
+    else if (nd == 4) launch_dia_nd<1, 4>(c, A, mode, xs, ys, b, st, part, counter, out);
+    else launch_dia_nd<1, 0>(c, A, mode, xs, ys, b, st, part, counter, out);
+  }
+}
+
 int launch_spmv(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const double* b,
                 const SolveState* st, double* part, unsigned int* counter, double* out) {
+  if (is_dia(A)) {
+    launch_dia(c, A, mode, xs, ys, b, st, part, counter, out);
+    RCG_LAUNCH_CHECK(c);
+    return RCG_OK;
+  }
   if (is_sell3(A)) {
     const int64_t nbr = A->n / 3;
     const int g = sell3_grid(c, nbr);
@@ -640,6 +936,20 @@ int launch_spmv(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const 
 }
 
 int launch_spmv_ind(Ctx* c, const rcg_csr* A, const SpmvArgs* dargs) {
+  if (is_dia(A)) {
+    const int g = dia_grid_for(c, A, 1, true);
+    const int nd = A->dia_count;
+    if (A->dia_block == 3) {
+      if (nd == 14) dia_kernel_ind<3, 14><<<g, kThreads, 0, c->stream>>>(dargs);
+      else dia_kernel_ind<3, 0><<<g, kThreads, 0, c->stream>>>(dargs);
+    } else {
+      if (nd == 3) dia_kernel_ind<1, 3><<<g, kThreads, 0, c->stream>>>(dargs);
+      else if (nd == 4) dia_kernel_ind<1, 4><<<g, kThreads, 0, c->stream>>>(dargs);
+      else dia_kernel_ind<1, 0><<<g, kThreads, 0, c->stream>>>(dargs);
+    }
+    RCG_LAUNCH_CHECK(c);
+    return RCG_OK;
+  }
   if (is_sell3(A)) {
     sell3_kernel_ind<<<sell3_grid(c, A->n / 3), kThreads, 0, c->stream>>>(dargs);
     RCG_LAUNCH_CHECK(c);
@@ -690,9 +1000,18 @@ void spmv_args_fill(const rcg_csr* A, SpmvArgs* s) {
   s->bro = A->bsr_row_offsets;
   s->bci = A->bsr_col_indices;
   s->bval = A->bsr_values;
+  s->dia_nd = A->dia_count;
+  s->dia_block = A->dia_block;
+  s->dia_offsets = A->dia_offsets;
+  s->dia_values = A->dia_values;
 }
 
 int spmv_partials(Ctx* c, const rcg_csr* A) {
+  if (is_dia(A)) {   // partial slots: the widest grid of the modes the solve launches
+    int g = dia_grid_for(c, A, 1, true);
+    for (int m = 0; m < 3; ++m) g = std::max(g, dia_grid_for(c, A, m, false));
+    return g;
+  }
   if (is_sell3(A)) return sell3_grid(c, A->n / 3);
   if (A->block == 3 && A->bsr_row_offsets) return bsr3_grid(c, A->n / 3);
   return spmv_grid(c, A, spmv_width(A));
@@ -894,5 +1213,102 @@ extern "C" int rcg_csr_block3_slice_build(rcg_ctx* ctx, const rcg_csr* A, const 
   sell3_fill_kernel<<<elementwise_grid(ctx, 32 * ((nbr + 31) / 32)), kThreads, 0, ctx->stream>>>(
       nbr, A->bsr_row_offsets, A->bsr_col_indices, A->bsr_values, chunk_offsets, sci, sval);
   RCG_LAUNCH_CHECK(ctx);
+  return RCG_OK;
+}
+
+extern "C" int rcg_csr_dia_analyze(rcg_ctx* ctx, const rcg_csr* A, int32_t B, int64_t* offs_host, int32_t* nd_host) {
+  if (!ctx || !A || !offs_host || !nd_host || (B != 1 && B != 3)) return RCG_ERR_CONTRACT;
+  *nd_host = 0;
+  if (A->n == 0 || A->n % B != 0) return RCG_OK;
+  char* sc = nullptr;
+  int rc = scratch(ctx, 4096, (void**)&sc);
+  if (rc) return rc;
+  unsigned long long* best = (unsigned long long*)sc;
+  int* bad = (int*)(sc + 64);
+  int64_t* doffs = (int64_t*)(sc + 1024);
+  RCG_CUDA(ctx, cudaMemsetAsync(sc, 0, 128, ctx->stream));
+  const int g = elementwise_grid(ctx, A->n);
+  if (A->row_offsets_64)
+    longest_row_kernel<int64_t><<<g, kThreads, 0, ctx->stream>>>(A->n, (const int64_t*)A->row_offsets, best);
+  else
+    longest_row_kernel<int32_t><<<g, kThreads, 0, ctx->stream>>>(A->n, (const int32_t*)A->row_offsets, best);
+  RCG_LAUNCH_CHECK(ctx);
+  unsigned long long hb = 0;
+  RCG_CUDA(ctx, cudaMemcpyAsync(&hb, best, sizeof(hb), cudaMemcpyDeviceToHost, ctx->stream));
+  RCG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  const int64_t len = (int64_t)(hb >> 32), row = (int64_t)(0xffffffffull - (hb & 0xffffffffull));
+  if (len <= 0 || len > 64 * B) return RCG_OK;
+  int64_t rs = 0;
+  if (A->row_offsets_64) RCG_CUDA(ctx, cudaMemcpy(&rs, (const int64_t*)A->row_offsets + row, 8, cudaMemcpyDeviceToHost));
+  else {
+    int32_t t = 0;
+    RCG_CUDA(ctx, cudaMemcpy(&t, (const int32_t*)A->row_offsets + row, 4, cudaMemcpyDeviceToHost));
+    rs = t;
+  }
+  std::vector<int32_t> cols(len);
+  RCG_CUDA(ctx, cudaMemcpy(cols.data(), A->col_indices + rs, len * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  std::vector<int64_t> offs;
+  // the longest row's offsets and their negations (a symmetric pattern has
+  // both; the first longest row of a small grid may sit on its boundary)
+  for (int32_t cc : cols) {
+    offs.push_back((int64_t)cc / B - row / B);
+    offs.push_back(row / B - (int64_t)cc / B);
+  }
+  std::sort(offs.begin(), offs.end());
+  offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
+  if ((int)offs.size() > DIA_MAX || std::find(offs.begin(), offs.end(), (int64_t)0) == offs.end()) return RCG_OK;
+  const int nd = (int)offs.size();
+  RCG_CUDA(ctx, cudaMemcpyAsync(doffs, offs.data(), nd * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+  if (A->row_offsets_64)
+    dia_verify_kernel<int64_t><<<g, kThreads, 0, ctx->stream>>>(A->n, B, (const int64_t*)A->row_offsets,
+                                                                A->col_indices, doffs, nd, bad);
+  else
+    dia_verify_kernel<int32_t><<<g, kThreads, 0, ctx->stream>>>(A->n, B, (const int32_t*)A->row_offsets,
+                                                                A->col_indices, doffs, nd, bad);
+  RCG_LAUNCH_CHECK(ctx);
+  int hbad = 1;
+  RCG_CUDA(ctx, cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  RCG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (hbad) return RCG_OK;
+  for (int d = 0; d < nd; ++d) offs_host[d] = offs[d];
+  *nd_host = nd;
+  return RCG_OK;
+}
+
+extern "C" int rcg_csr_dia_build(rcg_ctx* ctx, const rcg_csr* A, int32_t B, const int64_t* offs, int32_t nd_up,
+                                 double* U, int32_t* symmetric_host) {
+  if (!ctx || !A || !offs || !U || !symmetric_host || (B != 1 && B != 3) || nd_up < 1 || nd_up > DIA_MAX)
+    return RCG_ERR_CONTRACT;
+  *symmetric_host = 0;
+  if (A->n % B != 0) return set_error(ctx, RCG_ERR_CONTRACT, "n must be a multiple of the DIA block");
+  const int64_t nbr = A->n / B;
+  char* sc = nullptr;
+  int rc = scratch(ctx, 256, (void**)&sc);
+  if (rc) return rc;
+  unsigned long long* counts = (unsigned long long*)sc;
+  int* bad = (int*)(sc + 64);
+  RCG_CUDA(ctx, cudaMemsetAsync(sc, 0, 128, ctx->stream));
+  RCG_CUDA(ctx, cudaMemsetAsync(U, 0, sizeof(double) * (size_t)nd_up * B * B * nbr, ctx->stream));
+  const int g = elementwise_grid(ctx, A->n);
+  if (A->row_offsets_64) {
+    dia_fill_kernel<int64_t><<<g, kThreads, 0, ctx->stream>>>(A->n, B, (const int64_t*)A->row_offsets,
+                                                              A->col_indices, A->values, offs, nd_up, U, counts);
+    RCG_LAUNCH_CHECK(ctx);
+    dia_sym_kernel<int64_t><<<g, kThreads, 0, ctx->stream>>>(A->n, B, (const int64_t*)A->row_offsets,
+                                                             A->col_indices, A->values, offs, nd_up, U, bad);
+  } else {
+    dia_fill_kernel<int32_t><<<g, kThreads, 0, ctx->stream>>>(A->n, B, (const int32_t*)A->row_offsets,
+                                                              A->col_indices, A->values, offs, nd_up, U, counts);
+    RCG_LAUNCH_CHECK(ctx);
+    dia_sym_kernel<int32_t><<<g, kThreads, 0, ctx->stream>>>(A->n, B, (const int32_t*)A->row_offsets,
+                                                             A->col_indices, A->values, offs, nd_up, U, bad);
+  }
+  RCG_LAUNCH_CHECK(ctx);
+  unsigned long long hc[2] = {0, 1};
+  int hbad = 1;
+  RCG_CUDA(ctx, cudaMemcpyAsync(hc, counts, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
+  RCG_CUDA(ctx, cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  RCG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  *symmetric_host = (!hbad && hc[0] == hc[1]) ? 1 : 0;
   return RCG_OK;
 }

@@ -11,6 +11,9 @@ struct SpmvArgs {
   const int32_t* bro;
   const int32_t* bci;
   const double* bval;
+  int32_t dia_nd, dia_block;
+  const int64_t* dia_offsets;
+  const double* dia_values;
   ColSel xs, ys;
   const SolveState* st;
   double* part;

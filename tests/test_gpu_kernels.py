@@ -159,17 +159,16 @@ def test_block3_spmv_matches_scalar_csr(rng):
     A0 = problems.elasticity_q1(5, E=E)
     A = rcg.SparseSpdMatrix(A0.n, A0.row_offsets, A0.col_indices, A0.values, validate=False, use_block3=True)
     B = rcg.SparseSpdMatrix(A0.n, A0.row_offsets, A0.col_indices, A0.values, validate=False, use_block3=False)
-    assert A.device_csr().struct.block == 3
+    assert A.device_csr().struct.dia_count == 14 and A.device_csr().struct.dia_block == 3   # structured Q1: DIA
     assert B.device_csr().struct.block == 0
     x = rng.standard_normal(A.n)
     ya, yb = rcg.spmv(A, x), rcg.spmv(B, x)
     np.testing.assert_allclose(ya, yb, rtol=1e-13, atol=1e-13 * np.abs(yb).max())
     _spmv_close(A, x)
-    assert A.device_csr().struct.bsr_slice == 32        # sliced layout is the default
     # not block structured -> scalar path
     L0 = problems.assemble_diffusion(np.ones((6, 6)))
     L = rcg.SparseSpdMatrix(L0.n, L0.row_offsets, L0.col_indices, L0.values, validate=False, use_block3=True)
-    assert L.device_csr().struct.block == 0
+    assert L.device_csr().struct.block == 0 and L.device_csr().struct.dia_count == 3    # 5-point: scalar DIA
 
 
 @pytest.mark.parametrize("nelem", [1, 3, 7])
@@ -180,6 +179,7 @@ def test_sliced_block3_matches_plain_bsr(rng, monkeypatch, nelem):
     E = np.exp(rng.standard_normal((nelem,) * 3))
     A0 = problems.elasticity_q1(nelem, E=E)
     mk = lambda: rcg.SparseSpdMatrix(A0.n, A0.row_offsets, A0.col_indices, A0.values, validate=False)
+    monkeypatch.setenv("RCG_DIA", "0")
     S = mk()
     assert S.device_csr().struct.bsr_slice == 32
     monkeypatch.setenv("RCG_SELL", "0")
@@ -190,3 +190,59 @@ def test_sliced_block3_matches_plain_bsr(rng, monkeypatch, nelem):
         ys, yp = rcg.spmv(S, x), rcg.spmv(P, x)
         np.testing.assert_allclose(ys, yp, rtol=1e-14, atol=1e-14 * np.abs(yp).max())
         _spmv_close(S, x)
+
+
+def _mk(A0, **kw):
+    return rcg.SparseSpdMatrix(A0.n, A0.row_offsets, A0.col_indices, A0.values, validate=False, **kw)
+
+
+@pytest.mark.parametrize("kind", ["diff1d", "diff2d", "diff3d", "diff3d_flat", "q1_1", "q1_4", "q1_7"])
+def test_dia_matches_csr(rng, monkeypatch, kind):
+    """Symmetric block-DIA (stencils b = 1, structured Q1 b = 3): the same
+    product as scalar CSR on ragged grids (boundary rows, wrap-around
+    offsets, a single element, size-1 axes) for all three SpMV modes."""
+    if kind.startswith("diff"):
+        shape = {"diff1d": (37,), "diff2d": (9, 13), "diff3d": (5, 6, 7), "diff3d_flat": (4, 1, 9)}[kind]
+        A0 = problems.assemble_diffusion(rng.lognormal(0.0, 1.0, shape))
+        b = 1
+    else:
+        ne = int(kind.split("_")[1])
+        A0 = problems.elasticity_q1(ne, E=np.exp(rng.standard_normal((ne,) * 3)))
+        b = 3
+    D = _mk(A0)
+    assert D.device_csr().struct.dia_count > 0 and D.device_csr().struct.dia_block == b
+    C = _mk(A0, use_block3=False)
+    assert C.device_csr().struct.dia_count == 0
+    for _ in range(3):
+        x = rng.standard_normal(A0.n)
+        yd, yc = rcg.spmv(D, x), rcg.spmv(C, x)
+        np.testing.assert_allclose(yd, yc, rtol=1e-14, atol=1e-14 * np.abs(yc).max())
+        _spmv_close(D, x)
+    # modes 1 (solve loop) and 2 (initial residual) through a solve
+    bvec = rng.standard_normal(A0.n)
+    cfg = rcg.SolveConfig(tol=1e-10, max_iters=5000)
+    xs = []
+    for M in (D, C):
+        x, tr = rcg.apcg_solve(M, rcg.Preconditioner.jacobi(M), rcg.build_deflation(M, np.zeros((M.n, 0))), bvec, cfg)
+        xs.append((x, tr.iterations))
+    assert abs(xs[0][1] - xs[1][1]) <= max(1, 0.02 * xs[1][1])
+    assert np.linalg.norm(xs[0][0] - xs[1][0]) / np.linalg.norm(xs[1][0]) < 1e-8
+
+
+def test_dia_rejects_asymmetric_and_unstructured(rng):
+    """Not exactly symmetric (one lower entry perturbed) or not on a few
+    diagonals (random sparse SPD): no DIA copy, CSR/BSR path instead."""
+    A0 = problems.assemble_diffusion(rng.lognormal(0.0, 1.0, (6, 7)))
+    va = A0.values.copy()
+    rows = np.repeat(np.arange(A0.n), np.diff(A0.row_offsets))
+    k = np.flatnonzero(A0.col_indices < rows)[5]
+    va[k] = va[k] * (1 + 1e-15) + 1e-300
+    Asym = rcg.SparseSpdMatrix(A0.n, A0.row_offsets, A0.col_indices, va, validate=False)
+    assert Asym.device_csr().struct.dia_count == 0
+    R = rcg.SparseSpdMatrix.from_dense(orc_random_spd(rng, 60))
+    assert R.device_csr().struct.dia_count == 0
+
+
+def orc_random_spd(rng, n):
+    M = rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.1)
+    return M @ M.T + n * np.eye(n)

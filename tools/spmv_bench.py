@@ -33,5 +33,8 @@ t = e0.elapsed_time(e1) / N * 1e-3
 blk = h.struct.block
 byt = (8 * A.nnz + 4 * A.nnz / 9 + 4 * (A.n // 3 + 1) + 16 * A.n) if blk == 3 else (12 * A.nnz + 4 * (A.n + 1) + 16 * A.n)
 fmtname = ("sell3" if h.struct.bsr_slice == 32 else "bsr3") if blk == 3 else "csr"
+if h.struct.dia_count:
+    byt = 8 * h.struct.dia_count * h.struct.dia_block * A.n + 16 * A.n
+    fmtname = f"dia{h.struct.dia_block}x{h.struct.dia_count}"
 print(f"{which} fmt={fmtname} V={os.environ.get('RCG_SPMV_V','auto')} n={A.n} nnz={A.nnz} "
       f"t={t*1e6:.1f}us {byt/t/1e9:.0f} GB/s (algorithmic {byt/1e6:.0f} MB)")
