@@ -159,7 +159,7 @@ def test_block3_spmv_matches_scalar_csr(rng):
     A0 = problems.elasticity_q1(5, E=E)
     A = rcg.SparseSpdMatrix(A0.n, A0.row_offsets, A0.col_indices, A0.values, validate=False, use_block3=True)
     B = rcg.SparseSpdMatrix(A0.n, A0.row_offsets, A0.col_indices, A0.values, validate=False, use_block3=False)
-    assert A.device_csr().struct.dia_count == 14 and A.device_csr().struct.dia_block == 3   # structured Q1: DIA
+    assert A.device_csr().struct.block == 3 and A.device_csr().struct.dia_count == 0   # Q1: sliced 3x3 blocks
     assert B.device_csr().struct.block == 0
     x = rng.standard_normal(A.n)
     ya, yb = rcg.spmv(A, x), rcg.spmv(B, x)
@@ -201,6 +201,7 @@ def test_dia_matches_csr(rng, monkeypatch, kind):
     """Symmetric block-DIA (stencils b = 1, structured Q1 b = 3): the same
     product as scalar CSR on ragged grids (boundary rows, wrap-around
     offsets, a single element, size-1 axes) for all three SpMV modes."""
+    monkeypatch.setenv("RCG_DIA3", "1")
     if kind.startswith("diff"):
         shape = {"diff1d": (37,), "diff2d": (9, 13), "diff3d": (5, 6, 7), "diff3d_flat": (4, 1, 9)}[kind]
         A0 = problems.assemble_diffusion(rng.lognormal(0.0, 1.0, shape))
