@@ -317,11 +317,11 @@ def _maybe_block3(h, n, nnz, use_block3):
     if not use_block3:
         return
     blocky = n % 3 == 0 and nnz % 9 == 0 and nnz >= 9 * n // 3 * 2
-    # 3x3-block DIA halves the bytes of structured Q1 operators but its nine
-    # value streams per diagonal run at ~3.5 TB/s (vs 6.7 for the sliced
-    # blocks): about even at 64^3, slower at 160^3 -> opt-in (RCG_DIA3=1)
+    # 3x3-block DIA halves the bytes of structured Q1 operators; its nine
+    # value streams per diagonal run at ~4 TB/s (vs 6.7 for the sliced
+    # blocks), still 8-18% faster per SpMV at 64^3..160^3 (RCG_DIA3=0: off)
     dia_b = 3 if blocky else 1
-    if _os.environ.get("RCG_DIA", "1") != "0" and n > 0 and (dia_b == 1 or _os.environ.get("RCG_DIA3", "0") == "1"):
+    if _os.environ.get("RCG_DIA", "1") != "0" and n > 0 and (dia_b == 1 or _os.environ.get("RCG_DIA3", "1") == "1"):
         if h.add_dia(_lib.context(), dia_b):
             return
     if _os.environ.get("RCG_BSR", "1") != "0" and blocky:

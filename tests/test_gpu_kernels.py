@@ -159,7 +159,7 @@ def test_block3_spmv_matches_scalar_csr(rng):
     A0 = problems.elasticity_q1(5, E=E)
     A = rcg.SparseSpdMatrix(A0.n, A0.row_offsets, A0.col_indices, A0.values, validate=False, use_block3=True)
     B = rcg.SparseSpdMatrix(A0.n, A0.row_offsets, A0.col_indices, A0.values, validate=False, use_block3=False)
-    assert A.device_csr().struct.block == 3 and A.device_csr().struct.dia_count == 0   # Q1: sliced 3x3 blocks
+    assert A.device_csr().struct.dia_count == 14 and A.device_csr().struct.dia_block == 3   # structured Q1: DIA
     assert B.device_csr().struct.block == 0
     x = rng.standard_normal(A.n)
     ya, yb = rcg.spmv(A, x), rcg.spmv(B, x)
