@@ -322,9 +322,11 @@ def run_ours(args):
     box_copy = box_copy_gbps()
     d = stats[dom]
     achieved = d["bytes"] / d["seconds"] / 1e9 if d["seconds"] > 0 else 0.0
-    traffic = ncu_traffic().get(dom)
+    traffic_detail = ncu_traffic().get(dom)
+    traffic = traffic_detail.get("bytes") if isinstance(traffic_detail, dict) else None
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "frac": achieved / peak, "traffic": traffic, "traffic_detail": traffic_detail,
+                "peak_source": peak_src,
                 "share_of_kernel_time": d["seconds"] / tot_k if tot_k else None,
                 # context only (frac uses the driver-measured peak): this box's own copy
                 # bandwidth, measured like MEASURED_PEAKS.json (1 GiB copy_, best of 5)
