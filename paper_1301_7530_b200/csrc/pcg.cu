@@ -267,38 +267,22 @@ update_kernel(const IterArgs* __restrict__ ap, int init) {
   const int64_t p0 = r0 >> 1, p1 = r1 >> 1;
   double2* __restrict__ x2 = reinterpret_cast<double2*>(a.x);
   double2* __restrict__ r2 = reinterpret_cast<double2*>(a.r);
-  // UB pairs per thread per step: all their loads before any store (x / r
-  // may alias w / Aw for the compiler, which would serialize the steps)
-  constexpr int UB = 3;
-  for (int64_t pb = p0 + threadIdx.x; pb < p1; pb += UB * kThreads) {
-    double2 rv[UB], wv[UB], av[UB], xv[UB];
-#pragma unroll
-    for (int u = 0; u < UB; ++u) {
-      const int64_t pi = pb + u * kThreads;
-      if (pi < p1) {
-        rv[u] = r2[pi];
-        if (!init) {
-          wv[u] = reinterpret_cast<const double2*>(w)[pi];
-          av[u] = reinterpret_cast<const double2*>(aw)[pi];
-          xv[u] = x2[pi];
-        }
-      }
+#pragma unroll 2
+  for (int64_t pi = p0 + threadIdx.x; pi < p1; pi += kThreads) {
+    double2 rv = r2[pi];
+    if (!init) {
+      if (rh) reinterpret_cast<double2*>(rh)[pi] = rv;
+      const double2 wv = reinterpret_cast<const double2*>(w)[pi];
+      const double2 av = reinterpret_cast<const double2*>(aw)[pi];
+      double2 xv = x2[pi];
+      xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, wv.x));      // x = x + alpha w
+      xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, wv.y));
+      rv.x = __dsub_rn(rv.x, __dmul_rn(alpha, av.x));      // r = r - alpha Aw
+      rv.y = __dsub_rn(rv.y, __dmul_rn(alpha, av.y));
+      x2[pi] = xv;
+      r2[pi] = rv;
     }
-#pragma unroll
-    for (int u = 0; u < UB; ++u) {
-      const int64_t pi = pb + u * kThreads;
-      if (pi >= p1) break;
-      if (!init) {
-        if (rh) reinterpret_cast<double2*>(rh)[pi] = rv[u];
-        xv[u].x = __dadd_rn(xv[u].x, __dmul_rn(alpha, wv[u].x));   // x = x + alpha w
-        xv[u].y = __dadd_rn(xv[u].y, __dmul_rn(alpha, wv[u].y));
-        rv[u].x = __dsub_rn(rv[u].x, __dmul_rn(alpha, av[u].x));   // r = r - alpha Aw
-        rv[u].y = __dsub_rn(rv[u].y, __dmul_rn(alpha, av[u].y));
-        x2[pi] = xv[u];
-        r2[pi] = rv[u];
-      }
-      rr += rv[u].x * rv[u].x + rv[u].y * rv[u].y;
-    }
+    rr += rv.x * rv.x + rv.y * rv.y;
   }
   if ((r1 & 1) && threadIdx.x == 0) {
     const int64_t i = r1 - 1;

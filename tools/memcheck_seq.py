@@ -18,15 +18,15 @@ def run(name, seq, strat, cfg):
 
 import os
 cfg = rcg.SolveConfig(tol=1e-8, max_iters=3000)
-os.environ["RCG_DIA3"] = "1"
 el = list(problems.elasticity_sequence(6, 3, seed=0, kind="fixed"))
-assert el[0][0].device_csr().struct.dia_count == 14          # block-DIA SpMV (opt-in)
+assert el[0][0].device_csr().struct.dia_count == 14          # block-DIA SpMV
 run("elast6 srks dia", el, rcg.RecycleStrategy("srks", epsilon=1e-10, nc_limit=61), cfg)
-del os.environ["RCG_DIA3"]                                    # sliced 3x3 blocks (default)
+os.environ["RCG_DIA3"] = "0"                                  # sliced 3x3 blocks
 el = list(problems.elasticity_sequence(6, 3, seed=0, kind="fixed"))
 assert el[0][0].device_csr().struct.block == 3
 run("elast6 srks sell3", el, rcg.RecycleStrategy("srks", epsilon=1e-10, nc_limit=61), cfg)
 run("elast6 trks sell3", el, rcg.RecycleStrategy("trks", epsilon=1e-10, nc_limit=30), cfg)
+del os.environ["RCG_DIA3"]
 os.environ["RCG_DIA"] = "0"
 c1 = problems.shifted_laplacian_sequence(grid=24, count=3)  # scalar CSR
 run("lap24 srks csr", c1, rcg.RecycleStrategy("srks", epsilon=1e-10, nc_limit=200), cfg)
