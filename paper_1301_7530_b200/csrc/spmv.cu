@@ -369,6 +369,12 @@ constexpr int DIA_MAX = 64;
 #ifndef RCG_DIA3_K
 #define RCG_DIA3_K 4
 #endif
+#ifndef RCG_DIA1_K
+#define RCG_DIA1_K 8
+#endif
+#ifndef RCG_DIA1_MINB
+#define RCG_DIA1_MINB 4   // sweep (diff256 in-solve): 4 > 1, 2, 6, 8
+#endif
 #ifndef RCG_DIA3_MINB
 #define RCG_DIA3_MINB 2   // 128 registers: 2 CTAs/SM with 4 blocks (48 loads) in flight per thread
 #endif
@@ -402,7 +408,7 @@ __device__ __forceinline__ bool dia_body(int64_t nbr, int nd_rt, const int64_t* 
     // from a clamped valid address and adds fma(0, 0, acc).  K terms per
     // step load everything before the first FMA (in-order issue would
     // otherwise stall each step's loads behind the previous step's FMAs).
-    constexpr int K = B == 1 ? 8 : RCG_DIA3_K;
+    constexpr int K = B == 1 ? RCG_DIA1_K : RCG_DIA3_K;
     const int nt = 2 * nd - 1;
     double xd[B];   // x of this block row (the o = 0 block), kept for the (x, y) dot
 #pragma unroll(ND > 0 ? (2 * ND - 1 + K - 1) / K : 1)
@@ -469,7 +475,7 @@ __device__ __forceinline__ void dia_load_offsets(int nd, const int64_t* __restri
 }
 
 template <int B, int MODE, int ND>
-__global__ void __launch_bounds__(kThreads, B == 3 ? RCG_DIA3_MINB : 1)
+__global__ void __launch_bounds__(kThreads, B == 3 ? RCG_DIA3_MINB : RCG_DIA1_MINB)
 dia_kernel(int64_t nbr, int nd, const int64_t* __restrict__ offs, const double* __restrict__ U, ColSel xs, ColSel ys,
            const double* __restrict__ b, const SolveState* st, double* part, unsigned int* counter, double* out) {
   __shared__ int64_t so[DIA_MAX];
@@ -479,7 +485,7 @@ dia_kernel(int64_t nbr, int nd, const int64_t* __restrict__ offs, const double* 
 }
 
 template <int B, int ND>
-__global__ void __launch_bounds__(kThreads, B == 3 ? RCG_DIA3_MINB : 1) dia_kernel_ind(const SpmvArgs* __restrict__ sa) {
+__global__ void __launch_bounds__(kThreads, B == 3 ? RCG_DIA3_MINB : RCG_DIA1_MINB) dia_kernel_ind(const SpmvArgs* __restrict__ sa) {
   __shared__ int64_t so[DIA_MAX];
   const int nd = sa->dia_nd;
   dia_load_offsets(nd, sa->dia_offsets, so);
