@@ -552,9 +552,64 @@ colreduce_kernel(const IterArgs* __restrict__ ap) {
 // ---------------------------------------------------------------------------
 // K5: beta, w_{j+1} = z + beta w_j  (- W c' with c' = (AW^T w)/diag)
 
-// BATCH (no reorth): the finisher issues all its loads before any store;
-// with reorth the interleaved finisher keeps the W GEMV's registers
-template <int RPT, bool BATCH>
+// K5 without reorth: w_{j+1} = z + beta w_j, a pure stream.  A fixed grid of
+// one wave of resident CTAs walks row blocks of RPT rows per thread (all 2 RPT
+// loads of a block issued before its stores), so at 16.7 M rows 592 CTAs
+// instead of 4,096 arrive on the iteration counter.
+template <int RPT>
+__global__ void __launch_bounds__(kThreads)
+wupdate_plain_kernel(const IterArgs* __restrict__ ap) {
+  const IterArgs& a = *ap;
+  SolveState* st = a.st;
+  if (st->done) return;
+  const long long j = st->j;
+  const double rz_new = a.sums[a.rz_off];
+  const double rz_old = st->rz;
+  if (rz_new <= 0.0) {                                       // solver.py:279-280
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->failure = RCG_FAIL_RZ;
+      st->done = 1;
+    }
+    return;
+  }
+  const double beta = rz_new / rz_old;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.betas[j] = beta;
+  const double* __restrict__ z = a.Z.at(j + 1);
+  const double* __restrict__ wo = a.W.at(j);
+  double* __restrict__ wn = a.W.at(j + 1);
+  for (int64_t r0 = (int64_t)blockIdx.x * (kThreads * RPT); r0 < a.n; r0 += (int64_t)gridDim.x * (kThreads * RPT)) {
+    double zq[RPT], wq[RPT];
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int64_t i = r0 + threadIdx.x + q * kThreads;
+      zq[q] = i < a.n ? z[i] : 0.0;
+      wq[q] = i < a.n ? wo[i] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int64_t i = r0 + threadIdx.x + q * kThreads;
+      if (i < a.n) wn[i] = __dadd_rn(zq[q], __dmul_rn(beta, wq[q]));   // w = z + beta w
+    }
+  }
+  // the grid's last block advances the iteration (all blocks arrive once)
+  __shared__ bool g_last;
+  __syncthreads();  // + thread-0 fence (cumulative), see arrive_last
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int prev = atomicAdd(a.counters + 4, 1u);
+    g_last = (prev == gridDim.x - 1);
+    if (g_last) a.counters[4] = 0u;
+  }
+  __syncthreads();
+  if (g_last && threadIdx.x == 0) {
+    __threadfence();
+    st->rz = rz_new;
+    st->j = j + 1;
+    st->iterations = j + 1;
+  }
+}
+
+template <int RPT>
 __global__ void __launch_bounds__(kThreads)
 wupdate_kernel(const IterArgs* __restrict__ ap) {
   const IterArgs& a = *ap;
@@ -647,7 +702,7 @@ wupdate_kernel(const IterArgs* __restrict__ ap) {
       }
     }
   }
-  if (finisher && !BATCH) {
+  if (finisher) {
     const double* z = a.Z.at(j + 1);
     const double* wo = a.W.at(j);
     double* wn = a.W.at(j + 1);
@@ -656,29 +711,6 @@ wupdate_kernel(const IterArgs* __restrict__ ap) {
       const int64_t i = r0 + threadIdx.x + q * kThreads;
       if (i < a.n) {
         double v = __dadd_rn(z[i], __dmul_rn(beta, wo[i]));   // w = z + beta w
-        if (a.reorth) v = __dsub_rn(v, acc[q]);                // w -= W c'
-        wn[i] = v;
-      }
-    }
-  }
-  if (finisher && BATCH) {
-    const double* z = a.Z.at(j + 1);
-    const double* wo = a.W.at(j);
-    double* wn = a.W.at(j + 1);
-    // all 2 x RPT loads before the first store (wn may alias z / wo for the
-    // compiler: interleaved, every row would cost one HBM round trip)
-    double zq[RPT], wq[RPT];
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-      const int64_t i = r0 + threadIdx.x + q * kThreads;
-      zq[q] = i < a.n ? z[i] : 0.0;
-      wq[q] = i < a.n ? wo[i] : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-      const int64_t i = r0 + threadIdx.x + q * kThreads;
-      if (i < a.n) {
-        double v = __dadd_rn(zq[q], __dmul_rn(beta, wq[q]));  // w = z + beta w
         if (a.reorth) v = __dsub_rn(v, acc[q]);                // w -= W c'
         wn[i] = v;
       }
@@ -993,14 +1025,15 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   // row tiles: K3 needs 2 smem tiles only when reorthogonalizing and K2 one
   // only with an augmentation basis; otherwise tiles grow so the grid stays
   // at <= 8 CTAs/SM (few last-block arrivals even at n = 16.7 M)
-  auto big_tile = [&](int R0) {
-    const int64_t rmin = ceil_div(ceil_div(n, (int64_t)8 * c->num_sms), kThreads) * kThreads;
+  auto big_tile = [&](int R0, int per_sm) {
+    const int64_t rmin = ceil_div(ceil_div(n, (int64_t)per_sm * c->num_sms), kThreads) * kThreads;
     return (int)std::max<int64_t>(R0, rmin);
   };
-  const int R = reorth ? rows_per_block_for(c, n) : big_tile(rows_per_block_for(c, n));
+  // without reorth K3 is the lean 4-CTA/SM variant: at most one wave of tiles
+  const int R = reorth ? rows_per_block_for(c, n) : big_tile(rows_per_block_for(c, n), 4);
   const int nb = (int)std::max<int64_t>(1, ceil_div(n, R));
   static const int upd_tiles = env_int("RCG_UPD_TILES_PER_SM", 4);
-  const int Ru = n_c ? rows_per_block_for(c, n, upd_tiles) : big_tile(rows_per_block_for(c, n, upd_tiles));
+  const int Ru = n_c ? rows_per_block_for(c, n, upd_tiles) : big_tile(rows_per_block_for(c, n, upd_tiles), 8);
   const int nbu = (int)std::max<int64_t>(1, ceil_div(n, Ru));
   // K2b: exactly one wave of resident CTAs over all (tile, 8-column group)
   // pairs (a 1.3-wave grid ran its tail at a third of the SMs: 3.4 TB/s), so
@@ -1028,6 +1061,15 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   const int wu_rpt = (!reorth && ceil_div(n, (int64_t)kThreads * WU_RPT) > 8 * c->num_sms) ? 16
                      : (reorth ? wu_rpt_env : WU_RPT);
   const int wu_grid = (int)std::max<int64_t>(1, ceil_div(n, (int64_t)kThreads * wu_rpt));
+  static const int wu_plain_occ = [] {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wupdate_plain_kernel<8>, kThreads, 0) != cudaSuccess ||
+        occ < 1)
+      occ = 4;
+    return occ;
+  }();
+  const int wu_plain_grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>(ceil_div(n, (int64_t)kThreads * 8), (int64_t)wu_plain_occ * c->num_sms));
   // launch grids: the tile kernels grid-stride, capped at a few CTAs per SM
   const int cap_grid = 8 * c->num_sms;
   const int nb_l = nb, nbu_l = nbu, wu_l = std::min(wu_grid, cap_grid);
@@ -1342,14 +1384,11 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
       if ((rc2 = allreduce_h(H, c, gSum.ptr + a.rz_off, (size_t)(1 + (reorth ? 2 * (jj + 1) : 0))))) return rc2;
       if (direct) prof_begin(c, RCG_K_WUPDATE, 8.0 * nd * (3 + (reorth ? js : 0.0)));
       if (!reorth) {
-        if (wu_rpt == 16)
-          wupdate_kernel<16, true><<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
-        else
-          wupdate_kernel<WU_RPT, true><<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
+        wupdate_plain_kernel<8><<<wu_plain_grid, kThreads, 0, c->stream>>>(dargs);
       } else if (wu_rpt == 8) {
-        wupdate_kernel<8, false><<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
+        wupdate_kernel<8><<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
       } else {
-        wupdate_kernel<WU_RPT, false><<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
+        wupdate_kernel<WU_RPT><<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
       }
       RCG_LAUNCH_CHECK(c);
       if (direct) prof_end(c);
