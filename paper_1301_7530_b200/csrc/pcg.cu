@@ -90,7 +90,9 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* p, unsigned bytes) 
 // ahead of the warp's own loads: every PF_WIN steps each issues one
 // cp.async.bulk.prefetch.L2 of PF_WIN x 512 B of its column.  The register-
 // limited K3 (2 CTAs/SM) gets HBM requests in flight without holding
-// registers: 5.86 -> 6.4 TB/s in tools/gemv_layout_bench3.cu.
+// registers: 5.86 -> 6.4 TB/s in tools/gemv_layout_bench3.cu.  In the full
+// solve loop of the current build it no longer pays (config 2: K3 6.45 TB/s
+// with, 6.56 without, K5 also slightly faster): off unless RCG_PF=1.
 constexpr int PF_DIST = 2, PF_WIN = 4;
 
 // GEMV-T of one row tile: out[k*NV + v] = sum_rows M[:, k] v_v for k < ncols.
@@ -1221,7 +1223,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   RCG_CUDA(c, cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(smem_upd, 1024)));
   static const int pre_cg = env_int("RCG_PRE_CG", 8);
-  static const bool pre_pf = env_int("RCG_PF", 1) != 0;
+  static const bool pre_pf = env_int("RCG_PF", 0) != 0;
   auto pre = !reorth ? precond_kernel<8, false, false>
              : (pre_cg == 4 ? precond_kernel<4, false, true>
                             : (pre_cg == 2 ? precond_kernel<2, false, true>
