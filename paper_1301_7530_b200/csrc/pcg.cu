@@ -30,6 +30,9 @@
 
 namespace rcg {
 
+#ifndef RCG_ACTR_PIPE
+#define RCG_ACTR_PIPE 1
+#endif
 constexpr int CP_CHUNK = 4096;   // reorth coefficients staged per smem chunk
 constexpr int WU_RPT = 4;        // rows per thread in K5
 constexpr int NC_INLINE = 64;    // coarse solve recomputed per CTA up to this n_c
@@ -333,6 +336,38 @@ actr_kernel(const IterArgs* __restrict__ ap) {
   // each lane keeps CG + 2 LDG.128 in flight
   const double2* __restrict__ c2 = reinterpret_cast<const double2*>(cols);
   const int64_t ld2 = a.ldac >> 1;
+#if RCG_ACTR_PIPE
+  // software pipeline: the next row pair's CG + 2 loads are issued before
+  // this pair's FMAs, so a warp never waits a full round trip per step
+  double2 v[CG], y = make_double2(0.0, 0.0), d = make_double2(1.0, 1.0);
+  int64_t pi = pb + lane;
+  if (pi < pe) {
+#pragma unroll
+    for (int c = 0; c < CG; ++c) v[c] = __ldcs(c2 + (c < kc ? c : kc - 1) * ld2 + pi);
+    y = *reinterpret_cast<const double2*>(rr + 2 * pi);
+    if (inv) d = *reinterpret_cast<const double2*>(inv + 2 * pi);
+  }
+  for (; pi < pe; pi += 32) {
+    const int64_t pn = pi + 32;
+    double2 vn[CG], yn = make_double2(0.0, 0.0), dn = make_double2(1.0, 1.0);
+    if (pn < pe) {
+#pragma unroll
+      for (int c = 0; c < CG; ++c) vn[c] = __ldcs(c2 + (c < kc ? c : kc - 1) * ld2 + pn);
+      yn = *reinterpret_cast<const double2*>(rr + 2 * pn);
+      if (inv) dn = *reinterpret_cast<const double2*>(inv + 2 * pn);
+    }
+    if (inv) {
+      y.x = __dmul_rn(d.x, y.x);
+      y.y = __dmul_rn(d.y, y.y);
+    }
+#pragma unroll
+    for (int c = 0; c < CG; ++c) acc[c] += v[c].x * y.x + v[c].y * y.y;
+#pragma unroll
+    for (int c = 0; c < CG; ++c) v[c] = vn[c];
+    y = yn;
+    d = dn;
+  }
+#else
 #pragma unroll 1
   for (int64_t pi = pb + lane; pi < pe; pi += 32) {
     double2 v[CG];
@@ -347,6 +382,7 @@ actr_kernel(const IterArgs* __restrict__ ap) {
 #pragma unroll
     for (int c = 0; c < CG; ++c) acc[c] += v[c].x * y.x + v[c].y * y.y;
   }
+#endif
   if ((len & 1) && wid == kWarps - 1 && lane == 0) {
     const int64_t i = len - 1;
     const double y = inv ? __dmul_rn(inv[i], rr[i]) : rr[i];
