@@ -321,7 +321,11 @@ def _maybe_block3(h, n, nnz, use_block3):
     # value streams per diagonal run at ~4 TB/s (vs 6.7 for the sliced
     # blocks), still 8-18% faster per SpMV at 64^3..160^3 (RCG_DIA3=0: off)
     dia_b = 3 if blocky else 1
-    if _os.environ.get("RCG_DIA", "1") != "0" and n > 0 and (dia_b == 1 or _os.environ.get("RCG_DIA3", "1") == "1"):
+    # fewer bytes only pay when the operator streams from HBM: an L2-resident
+    # CSR (config 1, 1 MB) keeps the shorter-latency CSR kernel
+    streams = 12 * nnz > (32 << 20) or _os.environ.get("RCG_DIA_SMALL", "0") == "1"
+    if _os.environ.get("RCG_DIA", "1") != "0" and n > 0 and streams and \
+            (dia_b == 1 or _os.environ.get("RCG_DIA3", "1") == "1"):
         if h.add_dia(_lib.context(), dia_b):
             return
     if _os.environ.get("RCG_BSR", "1") != "0" and blocky:

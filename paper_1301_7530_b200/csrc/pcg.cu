@@ -937,31 +937,6 @@ struct Grow {
   size_t bytes = 0;
 };
 
-int grow(Ctx* c, Grow& g, int64_t need_cols, int64_t ld, int64_t used_cols) {
-  if (need_cols <= g.cols) return RCG_OK;
-  int64_t cols = std::max<int64_t>(need_cols, g.cols + g.cols / 2);
-  size_t bytes = sizeof(double) * (size_t)cols * ld;
-  double* p = (double*)c->pool->get(bytes);
-  if (!p) {
-    cols = need_cols;
-    bytes = sizeof(double) * (size_t)cols * ld;
-    p = (double*)c->pool->get(bytes);
-    if (!p)
-      return set_error(c, RCG_ERR_OOM, "out of device memory growing a Krylov history to %lld columns (%.2f GB)",
-                       (long long)cols, 8.0 * cols * ld / 1e9);
-  }
-  if (g.ptr) {
-    if (used_cols > 0)
-      RCG_CUDA(c, cudaMemcpyAsync(p, g.ptr, sizeof(double) * (size_t)used_cols * ld, cudaMemcpyDeviceToDevice,
-                                  c->stream));
-    RCG_CUDA(c, cudaStreamSynchronize(c->stream));
-    c->pool->put(g.ptr, g.bytes);
-  }
-  g.ptr = p;
-  g.cols = cols;
-  g.bytes = bytes;
-  return RCG_OK;
-}
 
 // Krylov history on a growable VA range: the pointer never moves, growth
 // maps more physical chunks (no copy, no peak)
@@ -1116,7 +1091,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
 
   // fixed-size device allocations
   SolveState* st = nullptr;
-  double *hist = nullptr, *r = nullptr, *sums = nullptr, *part_upd = nullptr, *part_z = nullptr;
+  double *hist = nullptr, *r = nullptr, *part_upd = nullptr, *part_z = nullptr;
   double* part_spmv = nullptr;
   double* s_ext = nullptr;
   unsigned int* counters = nullptr;

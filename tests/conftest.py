@@ -10,6 +10,13 @@ sys.path.insert(0, str(REPO / "tests"))
 
 GOLDEN = REPO / "tests" / "golden"
 
+# The symmetric-DIA SpMV is chosen in production only for operators that
+# stream from HBM (12 nnz > 32 MB); the parity suite's small grid operators
+# take it too, so every solver test also runs through that format (the CSR
+# and sliced-block paths keep their own explicit tests).
+import os  # noqa: E402
+os.environ.setdefault("RCG_DIA_SMALL", "1")
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA (B200) device and the built librcg.so")

@@ -72,6 +72,7 @@ def test_full_size_counts_and_symmetry(which, n, nnz):
         rng = np.random.Generator(np.random.Philox(0))
         A = problems.assemble_diffusion_device(rng.lognormal(0.0, 2.0, (256, 256, 256)))
     assert A.n == n and A.nnz == nnz
+    assert A.device_csr().struct.dia_count == (14 if which == "elast64" else 4)
     g = torch.Generator(device="cuda").manual_seed(0)
     x = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
     y = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)

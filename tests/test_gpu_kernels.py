@@ -247,3 +247,13 @@ def test_dia_rejects_asymmetric_and_unstructured(rng):
 def orc_random_spd(rng, n):
     M = rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.1)
     return M @ M.T + n * np.eye(n)
+
+
+def test_small_operators_keep_csr_in_production(monkeypatch):
+    """Without the test-suite override, an L2-resident operator (config-1
+    5-point 128^2: 1 MB of CSR) keeps the CSR kernel; the 256^3 7-point
+    operator (1.4 GB) takes the DIA one (test_full_size_counts_and_symmetry)."""
+    monkeypatch.delenv("RCG_DIA_SMALL", raising=False)
+    A, _ = problems.shifted_laplacian_sequence(count=1)[0]
+    h = A.device_csr().struct
+    assert h.dia_count == 0 and h.block == 0

@@ -17,6 +17,7 @@ def run(name, seq, strat, cfg):
     assert all(r.converged for r in rep.records) and not rep.aborted
 
 import os
+os.environ["RCG_DIA_SMALL"] = "1"                             # DIA for these small operators too
 cfg = rcg.SolveConfig(tol=1e-8, max_iters=3000)
 el = list(problems.elasticity_sequence(6, 3, seed=0, kind="fixed"))
 assert el[0][0].device_csr().struct.dia_count == 14          # block-DIA SpMV
