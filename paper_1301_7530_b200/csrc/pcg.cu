@@ -30,6 +30,13 @@
 
 namespace rcg {
 
+#ifndef RCG_PRE_MINB
+#define RCG_PRE_MINB 2
+#endif
+#ifndef RCG_GEMV_UNROLL
+#define RCG_GEMV_UNROLL 2
+#endif
+constexpr int kGemvUnroll = RCG_GEMV_UNROLL;
 #ifndef RCG_ACTR_PIPE
 #define RCG_ACTR_PIPE 1
 #endif
@@ -142,7 +149,7 @@ __device__ __forceinline__ void gemv_t_tile(const double* __restrict__ base, int
         if (PF && lane < CG && p_begin < p_end)
           bulk_prefetch_l2(cols + lane * ld + 2 * p_begin,
                            (unsigned)(16 * min((int64_t)32 * PF_DIST, p_end - p_begin)));
-#pragma unroll 2
+#pragma unroll(kGemvUnroll)
         for (int64_t pi = p_begin + lane; pi < p_end; pi += 32) {
           if (PF && lane < CG) {
             const int64_t step0 = pi - lane - p_begin;  // multiple of 32
@@ -442,7 +449,7 @@ coarse_kernel(const IterArgs* __restrict__ ap, int check_done) {
 // REO = false: the lean no-reorth variant (no GEMV code, so no 128-register
 // budget): 4 CTAs/SM keep enough row loads in flight for the z pass
 template <int CG, bool PF, bool REO>
-__global__ void __launch_bounds__(kThreads, REO ? 2 : 4)
+__global__ void __launch_bounds__(kThreads, REO ? RCG_PRE_MINB : 4)
 precond_kernel(const IterArgs* __restrict__ ap, int init) {
   const IterArgs& a = *ap;
   SolveState* st = a.st;
