@@ -554,8 +554,11 @@ precond_kernel(const IterArgs* __restrict__ ap, int init) {
   if (lead && arrive_last(a.counters + 2)) reduce_partials<kThreads>(a.part_z, gridDim.x, 1, a.sums + a.rz_off);
 }
 
-// K4: sums[rz_off+1+q] = sum_b part_reo[b][q], q < 2(j+1); 32 q per CTA step x 8
-// b-groups; grid-stride over q with a fixed grid so the launch is graph-replayable
+// K4: sums[rz_off+1+q] = sum_b part_reo[b][q], q < 2(j+1).  8 q per CTA step
+// x 32 tile slices: each thread adds ~nb/32 tile partials (loads batched 4 at
+// a time), then the 32 slice sums of each q are added in slice order (fixed
+// order: bitwise reproducible).  Grid-stride over q with a fixed grid so the
+// launch is graph-replayable.
 __global__ void __launch_bounds__(256)
 colreduce_kernel(const IterArgs* __restrict__ ap) {
   const IterArgs& a = *ap;
@@ -563,32 +566,30 @@ colreduce_kernel(const IterArgs* __restrict__ ap) {
   const long long j = a.st->j;
   const int nb = a.nb_pre;
   const int64_t Q = 2 * (j + 1);
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  __shared__ double sm[8][33];
-  for (int64_t q0 = (int64_t)blockIdx.x * 32; q0 < Q; q0 += (int64_t)gridDim.x * 32) {
-    const int64_t q = q0 + tx;
+  const int tq = threadIdx.x & 7, ts = threadIdx.x >> 3;   // q in step, tile slice (0..31)
+  __shared__ double sm[32][9];
+  for (int64_t q0 = (int64_t)blockIdx.x * 8; q0 < Q; q0 += (int64_t)gridDim.x * 8) {
+    const int64_t q = q0 + tq;
     double s = 0.0;
     if (q < Q) {
-      // 8 tiles' partials loaded per step before they are added (same order
-      // as a plain loop): 8 loads in flight instead of one L2 round trip each
       const double* __restrict__ pc = a.part_reo + q;
-      int b = ty;
-      for (; b + 56 < nb; b += 64) {
-        double v[8];
+      int b = ts;
+      for (; b + 96 < nb; b += 128) {
+        double v[4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldcg(pc + (size_t)(b + 8 * u) * a.reo_stride);
+        for (int u = 0; u < 4; ++u) v[u] = __ldcg(pc + (size_t)(b + 32 * u) * a.reo_stride);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) s += v[u];
+        for (int u = 0; u < 4; ++u) s += v[u];
       }
-      for (; b < nb; b += 8) s += __ldcg(pc + (size_t)b * a.reo_stride);
+      for (; b < nb; b += 32) s += __ldcg(pc + (size_t)b * a.reo_stride);
     }
-    sm[ty][tx] = s;
+    sm[ts][tq] = s;
     __syncthreads();
-    if (ty == 0 && q < Q) {
-      double t = sm[0][tx];
-#pragma unroll
-      for (int g = 1; g < 8; ++g) t += sm[g][tx];
-      a.sums[a.rz_off + 1 + q] = t;
+    if (threadIdx.x < 8 && q0 + threadIdx.x < Q) {
+      double t = 0.0;
+#pragma unroll 8
+      for (int g = 0; g < 32; ++g) t += sm[g][threadIdx.x];
+      a.sums[a.rz_off + 1 + q0 + threadIdx.x] = t;
     }
     __syncthreads();
   }
