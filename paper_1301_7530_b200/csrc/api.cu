@@ -27,6 +27,14 @@ static bool pool_guard();
 static void guard_release(void* p);
 static void* guard_alloc(size_t bytes);
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("RCG_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
 int scratch(Ctx* c, size_t bytes, void** out) {
   if (pool_guard()) {  // exact size + canary per call (see Pool::get)
     if (c->scratch) guard_release(c->scratch);

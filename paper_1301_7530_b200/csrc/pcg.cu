@@ -245,6 +245,7 @@ __device__ __forceinline__ void gemv_t_tile(const double* __restrict__ base, int
 
 __global__ void __launch_bounds__(kThreads)
 update_kernel(const IterArgs* __restrict__ ap, int init) {
+  pdl_wait();
   const IterArgs& a = *ap;
   SolveState* st = a.st;
   if (st->done) return;
@@ -322,6 +323,7 @@ update_kernel(const IterArgs* __restrict__ ap, int init) {
 // [tile][1 + n_c] rows; the last CTA reduces them in a fixed order.
 __global__ void __launch_bounds__(kThreads)
 actr_kernel(const IterArgs* __restrict__ ap) {
+  pdl_wait();
   const IterArgs& a = *ap;
   if (a.st->done) return;
   constexpr int CG = 8;
@@ -429,6 +431,7 @@ actr_kernel(const IterArgs* __restrict__ ap) {
 // Ginv, grid-stride over rows (fixed grid: graph-replayable for any n_c)
 __global__ void __launch_bounds__(kThreads)
 coarse_kernel(const IterArgs* __restrict__ ap, int check_done) {
+  pdl_wait();
   const IterArgs& a = *ap;
   if (check_done && a.st->done) return;
   const int lane = threadIdx.x & 31;
@@ -451,6 +454,7 @@ coarse_kernel(const IterArgs* __restrict__ ap, int check_done) {
 template <int CG, bool PF, bool REO>
 __global__ void __launch_bounds__(kThreads, REO ? RCG_PRE_MINB : 4)
 precond_kernel(const IterArgs* __restrict__ ap, int init) {
+  pdl_wait();
   const IterArgs& a = *ap;
   SolveState* st = a.st;
   if (st->done) return;
@@ -561,6 +565,7 @@ precond_kernel(const IterArgs* __restrict__ ap, int init) {
 // launch is graph-replayable.
 __global__ void __launch_bounds__(256)
 colreduce_kernel(const IterArgs* __restrict__ ap) {
+  pdl_wait();
   const IterArgs& a = *ap;
   if (a.st->done) return;
   const long long j = a.st->j;
@@ -605,6 +610,7 @@ colreduce_kernel(const IterArgs* __restrict__ ap) {
 template <int RPT>
 __global__ void __launch_bounds__(kThreads)
 wupdate_plain_kernel(const IterArgs* __restrict__ ap) {
+  pdl_wait();
   const IterArgs& a = *ap;
   SolveState* st = a.st;
   if (st->done) return;
@@ -658,6 +664,7 @@ wupdate_plain_kernel(const IterArgs* __restrict__ ap) {
 template <int RPT>
 __global__ void __launch_bounds__(kThreads)
 wupdate_kernel(const IterArgs* __restrict__ ap) {
+  pdl_wait();
   const IterArgs& a = *ap;
   SolveState* st = a.st;
   if (st->done) return;
@@ -1376,13 +1383,14 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
       if (direct) prof_end(c);
       if ((rc2 = allreduce_h(H, c, gSum.ptr, 1))) return rc2;
       if (direct) prof_begin(c, RCG_K_UPDATE, 8.0 * nd * (6 + (store ? 1 : 0)));
-      update_kernel<<<nbu_l, kThreads, 0, c->stream>>>(dargs, 0);
-      RCG_LAUNCH_CHECK(c);
+      RCG_CUDA(c, launch_k(update_kernel, dim3(nbu_l), dim3(kThreads), 0, c->stream, (const IterArgs*)dargs, 0));
+      c->launches++;
       if (direct) prof_end(c);
       if (n_c) {
         if (direct) prof_begin(c, RCG_K_ACTR, 8.0 * nd * (1 + jac + n_c));
-        actr_kernel<<<dim3(nta, (unsigned)ngr), kThreads, 0, c->stream>>>(dargs);
-        RCG_LAUNCH_CHECK(c);
+        RCG_CUDA(c, launch_k(actr_kernel, dim3(nta, (unsigned)ngr), dim3(kThreads), 0, c->stream,
+                             (const IterArgs*)dargs));
+        c->launches++;
         if (direct) prof_end(c);
       }
       if ((rc2 = allreduce_h(H, c, gSum.ptr + 1, (size_t)(1 + n_c)))) return rc2;
@@ -1392,26 +1400,28 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
         if (direct) prof_end(c);
       }
       if (direct) prof_begin(c, RCG_K_PRECOND, 8.0 * nd * (2 + jac + n_c + (reorth ? 1.0 + js : 0.0)));
-      pre<<<dim3(nb_l, pre_split), kThreads, smem_pre, c->stream>>>(dargs, 0);
-      RCG_LAUNCH_CHECK(c);
+      RCG_CUDA(c, launch_k(pre, dim3(nb_l, pre_split), dim3(kThreads), smem_pre, c->stream, (const IterArgs*)dargs, 0));
+      c->launches++;
       if (direct) prof_end(c);
       if (reorth) {
         if (direct) prof_begin(c, RCG_K_COLREDUCE, 8.0 * 2.0 * js * (nb + 1));
-        colreduce_kernel<<<cr_grid, 256, 0, c->stream>>>(dargs);
-        RCG_LAUNCH_CHECK(c);
+        RCG_CUDA(c, launch_k(colreduce_kernel, dim3(cr_grid), dim3(256), 0, c->stream, (const IterArgs*)dargs));
+        c->launches++;
         if (direct) prof_end(c);
       }
       // one packed allreduce: (r, z) and the 2(j+1) reorth dot products
       if ((rc2 = allreduce_h(H, c, gSum.ptr + a.rz_off, (size_t)(1 + (reorth ? 2 * (jj + 1) : 0))))) return rc2;
       if (direct) prof_begin(c, RCG_K_WUPDATE, 8.0 * nd * (3 + (reorth ? js : 0.0)));
-      if (!reorth) {
-        wupdate_plain_kernel<8><<<wu_plain_grid, kThreads, 0, c->stream>>>(dargs);
-      } else if (wu_rpt == 8) {
-        wupdate_kernel<8><<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
-      } else {
-        wupdate_kernel<WU_RPT><<<dim3(wu_grid, wu_split), kThreads, 0, c->stream>>>(dargs);
-      }
-      RCG_LAUNCH_CHECK(c);
+      if (!reorth)
+        RCG_CUDA(c, launch_k(wupdate_plain_kernel<8>, dim3(wu_plain_grid), dim3(kThreads), 0, c->stream,
+                             (const IterArgs*)dargs));
+      else if (wu_rpt == 8)
+        RCG_CUDA(c, launch_k(wupdate_kernel<8>, dim3(wu_grid, wu_split), dim3(kThreads), 0, c->stream,
+                             (const IterArgs*)dargs));
+      else
+        RCG_CUDA(c, launch_k(wupdate_kernel<WU_RPT>, dim3(wu_grid, wu_split), dim3(kThreads), 0, c->stream,
+                             (const IterArgs*)dargs));
+      c->launches++;
       if (direct) prof_end(c);
     }
     return RCG_OK;

@@ -104,6 +104,40 @@ int set_error(Ctx* c, int code, const char* fmt, ...);
 int scratch(Ctx* c, size_t bytes, void** out);
 
 // ---------------------------------------------------------------------------
+// Programmatic dependent launch (sm_90+): the iteration kernels are launched
+// with programmatic stream serialization, so a kernel's CTAs are scheduled
+// while the previous kernel's last CTA (its fixed-order reduction) is still
+// running; every such kernel starts with pdl_wait() (griddepcontrol.wait),
+// which blocks until the previous grid has completed and its writes are
+// visible -- the same ordering as a plain stream launch, minus the launch
+// latency.  griddepcontrol.wait is a no-op for a normally launched grid.
+// RCG_PDL=0 launches plainly.
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args... args) {
+  if (!pdl_enabled()) {
+    k<<<grid, block, smem, s>>>(args...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
+// ---------------------------------------------------------------------------
 // device helpers
 
 __device__ __forceinline__ double warp_sum(double v) {

@@ -340,6 +340,7 @@ sell3_kernel(int64_t nbr, const int32_t* __restrict__ off, const int32_t* __rest
 }
 
 __global__ void __launch_bounds__(kThreads, RCG_SELL_MINB) sell3_kernel_ind(const SpmvArgs* __restrict__ sa) {
+  pdl_wait();
   double d0, d1;
   if (sell3_body<1, RCG_SELL_U>(sa->n / 3, sa->bro, sa->bci, sa->bval, sa->xs, sa->ys, nullptr, sa->st, d0, d1))
     spmv_epilogue<1>(d0, d1, sa->part, sa->counter, sa->out);
@@ -486,6 +487,7 @@ dia_kernel(int64_t nbr, int nd, const int64_t* __restrict__ offs, const double* 
 
 template <int B, int ND>
 __global__ void __launch_bounds__(kThreads, B == 3 ? RCG_DIA3_MINB : RCG_DIA1_MINB) dia_kernel_ind(const SpmvArgs* __restrict__ sa) {
+  pdl_wait();
   __shared__ int64_t so[DIA_MAX];
   const int nd = sa->dia_nd;
   dia_load_offsets(nd, sa->dia_offsets, so);
@@ -664,11 +666,13 @@ bsr3_kernel(int64_t nbr, const int32_t* __restrict__ bro, const int32_t* __restr
 // iteration, batch and solve of a sequence (see pcg.cu).
 template <typename RO, int V>
 __global__ void __launch_bounds__(kThreads, RCG_SPMV_MINB) spmv_kernel_ind(const SpmvArgs* __restrict__ sa) {
+  pdl_wait();
   spmv_body<RO, V, 1>(sa->n, (const RO*)sa->ro, sa->ci, sa->va, sa->xs, sa->ys, nullptr, sa->st, sa->part,
                       sa->counter, sa->out);
 }
 
 __global__ void __launch_bounds__(kThreads, RCG_SPMV_MINB) bsr3_kernel_ind(const SpmvArgs* __restrict__ sa) {
+  pdl_wait();
   bsr3_body<1>(sa->n / 3, sa->bro, sa->bci, sa->bval, sa->xs, sa->ys, nullptr, sa->st, sa->part, sa->counter,
                sa->out);
 }
@@ -948,59 +952,32 @@ int launch_spmv(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const 
 }
 
 int launch_spmv_ind(Ctx* c, const rcg_csr* A, const SpmvArgs* dargs) {
+  // one solve-loop kernel per stream format, launched with PDL (launch_k)
+  void (*k)(const SpmvArgs*) = nullptr;
+  int grid = 1;
   if (is_dia(A)) {
-    const int g = dia_grid_for(c, A, 1, true);
+    grid = dia_grid_for(c, A, 1, true);
     const int nd = A->dia_count;
-    if (A->dia_block == 3) {
-      if (nd == 14) dia_kernel_ind<3, 14><<<g, kThreads, 0, c->stream>>>(dargs);
-      else dia_kernel_ind<3, 0><<<g, kThreads, 0, c->stream>>>(dargs);
-    } else {
-      if (nd == 3) dia_kernel_ind<1, 3><<<g, kThreads, 0, c->stream>>>(dargs);
-      else if (nd == 4) dia_kernel_ind<1, 4><<<g, kThreads, 0, c->stream>>>(dargs);
-      else dia_kernel_ind<1, 0><<<g, kThreads, 0, c->stream>>>(dargs);
-    }
-    RCG_LAUNCH_CHECK(c);
-    return RCG_OK;
-  }
-  if (is_sell3(A)) {
-    sell3_kernel_ind<<<sell3_grid(c, A->n / 3), kThreads, 0, c->stream>>>(dargs);
-    RCG_LAUNCH_CHECK(c);
-    return RCG_OK;
-  }
-  if (A->block == 3 && A->bsr_row_offsets) {
-    bsr3_kernel_ind<<<bsr3_grid(c, A->n / 3), kThreads, 0, c->stream>>>(dargs);
-    RCG_LAUNCH_CHECK(c);
-    return RCG_OK;
-  }
-  const int V = spmv_width(A);
-  const int grid = spmv_grid(c, A, V);
-#define RCG_IND_CASE(RO, VV)                                                   \
-  case VV:                                                                     \
-    spmv_kernel_ind<RO, VV><<<grid, kThreads, 0, c->stream>>>(dargs);          \
-    break;
-  if (A->row_offsets_64) {
-    switch (V) {
-      RCG_IND_CASE(int64_t, 1)
-      RCG_IND_CASE(int64_t, 2)
-      RCG_IND_CASE(int64_t, 4)
-      RCG_IND_CASE(int64_t, 8)
-      RCG_IND_CASE(int64_t, 16)
-      default:
-        spmv_kernel_ind<int64_t, 32><<<grid, kThreads, 0, c->stream>>>(dargs);
-    }
+    if (A->dia_block == 3) k = nd == 14 ? dia_kernel_ind<3, 14> : dia_kernel_ind<3, 0>;
+    else k = nd == 3 ? dia_kernel_ind<1, 3> : (nd == 4 ? dia_kernel_ind<1, 4> : dia_kernel_ind<1, 0>);
+  } else if (is_sell3(A)) {
+    grid = sell3_grid(c, A->n / 3);
+    k = sell3_kernel_ind;
+  } else if (A->block == 3 && A->bsr_row_offsets) {
+    grid = bsr3_grid(c, A->n / 3);
+    k = bsr3_kernel_ind;
   } else {
-    switch (V) {
-      RCG_IND_CASE(int32_t, 1)
-      RCG_IND_CASE(int32_t, 2)
-      RCG_IND_CASE(int32_t, 4)
-      RCG_IND_CASE(int32_t, 8)
-      RCG_IND_CASE(int32_t, 16)
-      default:
-        spmv_kernel_ind<int32_t, 32><<<grid, kThreads, 0, c->stream>>>(dargs);
-    }
+    const int V = spmv_width(A);
+    grid = spmv_grid(c, A, V);
+    if (A->row_offsets_64)
+      k = V == 1 ? spmv_kernel_ind<int64_t, 1> : V == 2 ? spmv_kernel_ind<int64_t, 2> : V == 4 ? spmv_kernel_ind<int64_t, 4>
+        : V == 8 ? spmv_kernel_ind<int64_t, 8> : V == 16 ? spmv_kernel_ind<int64_t, 16> : spmv_kernel_ind<int64_t, 32>;
+    else
+      k = V == 1 ? spmv_kernel_ind<int32_t, 1> : V == 2 ? spmv_kernel_ind<int32_t, 2> : V == 4 ? spmv_kernel_ind<int32_t, 4>
+        : V == 8 ? spmv_kernel_ind<int32_t, 8> : V == 16 ? spmv_kernel_ind<int32_t, 16> : spmv_kernel_ind<int32_t, 32>;
   }
-#undef RCG_IND_CASE
-  RCG_LAUNCH_CHECK(c);
+  RCG_CUDA(c, launch_k(k, dim3(grid), dim3(kThreads), 0, c->stream, dargs));
+  c->launches++;
   return RCG_OK;
 }
 
