@@ -74,9 +74,10 @@ typedef struct {
   int32_t pad1;
   const int64_t* dia_offsets;       /* [dia_count] upper block-diagonal offsets,
                                        ascending, dia_offsets[0] = 0 (device) */
-  const double* dia_values;         /* [dia_count][b*b][n/b]: entry (i, jj) of
-                                       block (p, p + off_d) at
-                                       ((d*b + i)*b + jj)*(n/b) + p; 0 = absent */
+  const double* dia_values;         /* dia_count * b*b * 32*ceil(n/b/32): entry
+                                       q = i*b + jj of block (p, p + off_d) at
+                                       ((d*T + p/32)*b*b + q)*32 + p%32,
+                                       T = ceil(n/b/32); 0 = absent */
 } rcg_csr;
 
 /* Deflation operator P = I - C G^{-1} (AC)^T, G = C^T A C (DeflationOperator,
@@ -246,7 +247,8 @@ int rcg_gen_elasticity_fill(rcg_ctx* ctx, int64_t nelem, const double* Ke, const
  * every entry; *nd_host = their count (0: not DIA-structured; at most 64),
  * offs_host[0..nd) ascending (synchronizes).
  * build: offs = the upper offsets (>= 0, ascending, device), nd_up of them;
- * fills U[nd_up][b*b][n/b] and checks exact symmetry (values and pattern):
+ * fills U (nd_up * b*b * 32*ceil(n/b/32) doubles, layout at dia_values) and
+ * checks exact symmetry (values and pattern):
  * *symmetric_host = 1 when the copy reproduces A, else 0 (do not use it). */
 int rcg_csr_dia_analyze(rcg_ctx* ctx, const rcg_csr* A, int32_t b, int64_t* offs_host, int32_t* nd_host);
 int rcg_csr_dia_build(rcg_ctx* ctx, const rcg_csr* A, int32_t b, const int64_t* offs, int32_t nd_up, double* U,

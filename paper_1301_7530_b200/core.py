@@ -101,7 +101,7 @@ class _DevCsr:
         if not up or 8.0 * len(up) * b * n > 8.0 * nnz + 4.0 * nnz / (9 if b == 3 else 1):
             return False
         doffs = torch.tensor(up, dtype=torch.int64, device="cuda")
-        dvals = torch.empty(len(up) * b * n, dtype=torch.float64, device="cuda")
+        dvals = torch.empty(len(up) * b * b * 32 * ((n // b + 31) // 32), dtype=torch.float64, device="cuda")
         sym = _lib.C.c_int32(0)
         ctx.check(ctx.lib.rcg_csr_dia_build(ctx.h, _lib.C.byref(self.struct), b, _lib.ptr(doffs), len(up),
                                             _lib.ptr(dvals), _lib.C.byref(sym)), "dia_build")
