@@ -23,6 +23,8 @@
 #include "comm.cuh"
 #include "vmm.cuh"
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cstdlib>
 #include <chrono>
@@ -30,6 +32,9 @@
 
 namespace rcg {
 
+#ifndef RCG_CG_SYNC
+#define RCG_CG_SYNC 0
+#endif
 #ifndef RCG_PRE_MINB
 #define RCG_PRE_MINB 2
 #endif
@@ -601,6 +606,288 @@ colreduce_kernel(const IterArgs* __restrict__ ap) {
 }
 
 // ---------------------------------------------------------------------------
+// Persistent solve loop for small operators (n = 16,384 is
+// L2-resident and each iteration is 3-4 dependent reductions, so six kernel
+// launches and their last-block tails dominate).  One cooperative grid of one
+// CTA per SM runs up to B iterations; block b owns the contiguous rows
+// [b R, (b+1) R).  Five grid-wide barriers per iteration replace the launch
+// boundaries; every block re-derives alpha, ||r||, beta and the convergence /
+// failure decisions from the same partial rows in the same fixed order, so
+// all blocks take identical branches and write identical bits (block 0 writes
+// the trace).  Same arithmetic as K1-K5 (CSR SpMV with sequential row sums,
+// explicitly rounded updates); used only when n <= RCG_SMALL_N, n_c <= 64,
+// no r history, no Krylov cap and no sharding.
+//   sp row b: [0] (w, Aw)  [1] ||r||^2  [2, 2+n_c) AC^T y  [2+n_c] (r, z)
+
+constexpr int SMALL_ROWS = 512;   // max rows per block (n <= 148 * 512)
+
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int& gen) {
+#if RCG_CG_SYNC
+  (void)bar;
+  (void)gen;
+  cooperative_groups::this_grid().sync();
+  return;
+#endif
+  // sense-free generation barrier over gridDim.x co-resident blocks
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ++gen;
+    __threadfence();
+    const unsigned int target = gen * gridDim.x;
+    atomicAdd(bar, 1u);
+    while (true) {
+      unsigned int v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      if ((int)(v - target) >= 0) break;
+    }
+  }
+  __syncthreads();
+}
+
+// fixed-order sum over the G block rows of column `col` (stride `ld`), same
+// bits in every block: lanes stride the rows, then a fixed shuffle tree
+__device__ __forceinline__ double grid_sum_col(const double* part, int ld, int col, int G) {
+  double s = 0.0;
+  for (int b = threadIdx.x & 31; b < G; b += 32) s += __ldcg(part + (size_t)b * ld + col);
+  return warp_sum(s);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+small_solve_kernel(const IterArgs* __restrict__ ap, double* sp, int sps, unsigned int* bar, long long B) {
+  const IterArgs& a = *ap;
+  SolveState* st = a.st;
+  const int G = gridDim.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t n = a.n, R = (n + G - 1) / G;
+  const int64_t r0 = min(n, (int64_t)blockIdx.x * R), r1 = min(n, r0 + R);
+  const int64_t len = r1 - r0;
+  const int32_t* __restrict__ ci = a.spmv.ci;
+  const double* __restrict__ va = a.spmv.va;
+  __shared__ double ys[SMALL_ROWS], zs[SMALL_ROWS], wsh[SMALL_ROWS];
+  __shared__ double ssh[NC_INLINE];
+  __shared__ double cp[CP_CHUNK];
+  __shared__ double red[kWarps];
+  __shared__ double bc[4];
+  unsigned int gen = 0;
+  if (threadIdx.x == 0) gen = __ldcg(bar) / G;   // barrier generations already completed
+  const int ncs = (int)a.n_c;
+  for (long long it = 0; it < B; ++it) {
+    if (__ldcg(&st->done)) return;
+    const long long j = __ldcg(&st->j);
+    const double rz = __ldcg(&st->rz);
+    const double* __restrict__ w = a.W.at(j);
+    double* __restrict__ aw = a.AW.at(j);
+    // ---- K1: Aw_j = A w_j (thread per row, CSR, sequential row sum); (w, Aw)
+    double d0 = 0.0;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
+      const int64_t ks = ((const int32_t*)a.spmv.ro)[i], ke = ((const int32_t*)a.spmv.ro)[i + 1];
+      double acc = 0.0;
+      for (int64_t k = ks; k < ke; ++k) acc += va[k] * __ldcg(w + ci[k]);
+      aw[i] = acc;
+      d0 += __ldcg(w + i) * acc;
+    }
+    d0 = block_sum<kThreads>(d0, red);
+    if (threadIdx.x == 0) sp[(size_t)blockIdx.x * sps] = d0;
+    grid_barrier(bar, gen);
+    // ---- K2: alpha; x += alpha w; r -= alpha Aw; ||r||^2; AC^T y (own rows)
+    if (wid == 0) {
+      const double t = grid_sum_col(sp, sps, 0, G);
+      if (lane == 0) bc[0] = t;
+    }
+    __syncthreads();
+    const double wAw = bc[0];
+    if (wAw <= 0.0) {                                        // solver.py:244-245
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->failure = RCG_FAIL_WAW;
+        st->done = 1;
+      }
+      return;
+    }
+    const double alpha = rz / wAw;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.alphas[j] = alpha;
+      a.rz_hist[j] = rz;
+      if (a.waw_diag) a.waw_diag[j] = wAw;
+    }
+    double rr = 0.0;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
+      const double xi = __dadd_rn(a.x[i], __dmul_rn(alpha, w[i]));     // x = x + alpha w
+      const double ri = __dsub_rn(a.r[i], __dmul_rn(alpha, __ldcg(aw + i)));   // r = r - alpha Aw
+      a.x[i] = xi;
+      a.r[i] = ri;
+      rr += ri * ri;
+      ys[i - r0] = a.inv_diag ? __dmul_rn(a.inv_diag[i], ri) : ri;
+      wsh[i - r0] = w[i];
+    }
+    rr = block_sum<kThreads>(rr, red);
+    if (threadIdx.x == 0) sp[(size_t)blockIdx.x * sps + 1] = rr;
+    for (int c = wid; c < ncs; c += kWarps) {                // AC^T y over the block's rows
+      const double* col = a.AC + (int64_t)c * a.ldac;
+      double t = 0.0;
+      for (int64_t q = lane; q < len; q += 32) t += col[r0 + q] * ys[q];
+      t = warp_sum(t);
+      if (lane == 0) sp[(size_t)blockIdx.x * sps + 2 + c] = t;
+    }
+    grid_barrier(bar, gen);
+    // ---- K3: ||r|| test; s = G^{-1} u; z = M^{-1} r - C s; (r, z); reorth partials
+    if (wid == 0) {
+      const double t = grid_sum_col(sp, sps, 1, G);
+      if (lane == 0) bc[1] = t;
+    }
+    for (int c = wid; c < ncs; c += kWarps) {
+      const double t = grid_sum_col(sp, sps, 2 + c, G);
+      if (lane == 0) cp[c] = t;                               // u = AC^T y
+    }
+    __syncthreads();
+    const double rnorm = sqrt(bc[1]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.rnorms[j + 1] = rnorm;
+    if (rnorm <= st->tol_abs) {                               // solver.py:273
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->converged = 1;
+        st->iterations = j + 1;
+        st->done = 1;
+      }
+      return;
+    }
+    for (int i = threadIdx.x; i < ncs; i += kThreads) {      // s = Ginv u, fixed order
+      const double* g = a.Ginv + (int64_t)i * ncs;
+      double acc = 0.0;
+      for (int k = 0; k < ncs; ++k) acc += g[k] * cp[k];
+      ssh[i] = acc;
+    }
+    __syncthreads();
+    double* __restrict__ z = a.Z.at(j + 1);
+    double rzp = 0.0;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
+      const double ri = a.r[i];
+      double zi = a.inv_diag ? __dmul_rn(a.inv_diag[i], ri) : ri;
+      if (ncs) {
+        double cs = 0.0;
+        for (int c = 0; c < ncs; ++c) cs += a.C[(int64_t)c * a.ldc + i] * ssh[c];
+        zi = __dsub_rn(zi, cs);                               // y - C s  (solver.py:91)
+      }
+      z[i] = zi;
+      zs[i - r0] = zi;
+      rzp += ri * zi;
+    }
+    rzp = block_sum<kThreads>(rzp, red);
+    if (threadIdx.x == 0) sp[(size_t)blockIdx.x * sps + 2 + ncs] = rzp;
+    if (a.reorth) {                                           // AW^T z, AW^T w_j over own rows
+      // warp per group of 8 columns, lanes over the block's rows: 8 loads in
+      // flight per lane and row step, one shuffle tree per column
+      constexpr int SG = 8;
+      double* pr = a.part_reo + (size_t)blockIdx.x * a.reo_stride;
+      for (long long k0 = (long long)wid * SG; k0 <= j; k0 += (long long)kWarps * SG) {
+        double t0[SG], t1[SG];
+#pragma unroll
+        for (int u = 0; u < SG; ++u) t0[u] = t1[u] = 0.0;
+        const double* col = a.AW.base + (k0 + a.AW.shift) * a.AW.ld + r0;
+        for (int64_t q = lane; q < len; q += 32) {
+          const double zq = zs[q], wq = wsh[q];
+          double v[SG];
+#pragma unroll
+          for (int u = 0; u < SG; ++u) v[u] = k0 + u <= j ? __ldcg(col + u * a.AW.ld + q) : 0.0;
+#pragma unroll
+          for (int u = 0; u < SG; ++u) {
+            t0[u] += v[u] * zq;
+            t1[u] += v[u] * wq;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < SG; ++u) {
+          t0[u] = warp_sum(t0[u]);
+          t1[u] = warp_sum(t1[u]);
+          if (lane == 0 && k0 + u <= j) {
+            pr[2 * (k0 + u)] = t0[u];
+            pr[2 * (k0 + u) + 1] = t1[u];
+          }
+        }
+      }
+    }
+    grid_barrier(bar, gen);
+    // ---- K4: (r, z); reorth coefficients, column q reduced by block q mod G
+    if (wid == 0) {
+      const double t = grid_sum_col(sp, sps, 2 + ncs, G);
+      if (lane == 0) bc[2] = t;
+    }
+    if (a.reorth) {
+      const long long Q = 2 * (j + 1);
+      for (long long q = (long long)blockIdx.x * kWarps + wid; q < Q; q += (long long)G * kWarps) {
+        const double t = grid_sum_col(a.part_reo, (int)a.reo_stride, (int)q, G);
+        if (lane == 0) a.sums[a.rz_off + 1 + q] = t;
+      }
+    }
+    __syncthreads();
+    const double rz_new = bc[2];
+    if (rz_new <= 0.0) {                                      // solver.py:279-280
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->failure = RCG_FAIL_RZ;
+        st->done = 1;
+      }
+      return;
+    }
+    const double beta = rz_new / rz;
+    if (a.reorth) grid_barrier(bar, gen);
+    // ---- K5: w_{j+1} = z + beta w_j - W ((AW^T (z + beta w)) / diag)
+    double* __restrict__ wn = a.W.at(j + 1);
+    const double* red2 = a.sums + a.rz_off + 1;
+    double acc[2] = {0.0, 0.0};
+    if (a.reorth) {
+      for (long long k0 = 0; k0 <= j; k0 += CP_CHUNK) {
+        const long long kn = min((long long)CP_CHUNK, j + 1 - k0);
+        __syncthreads();
+        for (long long k = threadIdx.x; k < kn; k += kThreads) {
+          const long long kk = k0 + k;
+          cp[k] = (__ldcg(red2 + 2 * kk) + beta * __ldcg(red2 + 2 * kk + 1)) / __ldcg(a.waw_diag + kk);
+        }
+        __syncthreads();
+        // 8 columns per step, all 16 loads issued before the FMAs (in-order
+        // issue would otherwise pay one L2 round trip per column)
+        const double* colb = a.W.base + (k0 + a.W.shift) * a.W.ld;
+        long long k = 0;
+        for (; k + 8 <= kn; k += 8) {
+          double v[8][2];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int64_t i = r0 + threadIdx.x + q * kThreads;
+              v[u][q] = i < r1 ? __ldcg(colb + (k + u) * a.W.ld + i) : 0.0;
+            }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) acc[q] += v[u][q] * cp[k + u];
+        }
+        for (; k < kn; ++k) {
+          const double ck = cp[k];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int64_t i = r0 + threadIdx.x + q * kThreads;
+            if (i < r1) acc[q] += __ldcg(colb + k * a.W.ld + i) * ck;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int64_t i = r0 + threadIdx.x + q * kThreads;
+      if (i < r1) {
+        double v = __dadd_rn(zs[i - r0], __dmul_rn(beta, wsh[i - r0]));   // w = z + beta w
+        if (a.reorth) v = __dsub_rn(v, acc[q]);                          // w -= W c'
+        wn[i] = v;
+      }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.betas[j] = beta;
+      st->rz = rz_new;
+      st->j = j + 1;
+      st->iterations = j + 1;
+    }
+    grid_barrier(bar, gen);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K5: beta, w_{j+1} = z + beta w_j  (- W c' with c' = (AW^T w)/diag)
 
 // K5 without reorth: w_{j+1} = z + beta w_j, a pure stream.  A fixed grid of
@@ -1154,6 +1441,11 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   if (store && (rc = hist_init(c, gR, full_cols, init_cols, ld))) return fail(rc);
 
   auto reo_cols = [&]() { return gAW.cols; };
+  // persistent cooperative solve loop for small operators (small_solve_kernel)
+  const int64_t small_n = env_int("RCG_SMALL_N", 65536);   // read per solve (tests switch paths)
+  const bool small = !H && n <= small_n && n <= (int64_t)c->num_sms * SMALL_ROWS && n_c <= NC_INLINE && !store &&
+                     !zcap && !A->row_offsets_64 && n > 0;
+  const int small_G = small ? c->num_sms : 0;
   auto ensure_sums = [&](void) -> int {
     const int64_t need = 8 + n_c + 1 + 2 * reo_cols() + 8;
     if (gSum.cols < need) {
@@ -1170,7 +1462,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
       gSum.bytes = sizeof(double) * need;
     }
     if (reorth) {
-      const int64_t needp = (int64_t)nb * 2 * reo_cols();
+      const int64_t needp = (int64_t)std::max(nb, small_G) * 2 * reo_cols();
       if (gPR.cols < needp) {
         if (gPR.ptr) {
           RCG_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -1189,6 +1481,14 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   if (!c->dargs && cudaMalloc(&c->dargs, 4096) != cudaSuccess) return fail(set_error(c, RCG_ERR_OOM, "args"));
   static_assert(sizeof(IterArgs) <= 4096, "IterArgs too large");
   IterArgs* dargs = (IterArgs*)c->dargs;
+  double* small_sp = nullptr;
+  unsigned int* small_bar = nullptr;
+  const int small_sps = 3 + (int)n_c;
+  if (small) {
+    if ((rc = alloc(sizeof(double) * (size_t)small_G * small_sps + 256, (void**)&small_sp))) return fail(rc);
+    small_bar = (unsigned int*)(small_sp + (size_t)small_G * small_sps);
+    RCG_CUDA(c, cudaMemsetAsync(small_bar, 0, 64, c->stream));
+  }
   IterArgs a{};
   auto refresh = [&]() {
     a.n = n;
@@ -1453,7 +1753,14 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
       RCG_CUDA(c, refresh());
     }
     const bool graph_ok = use_graphs && !c->profiling && !H;
-    if (graph_ok) {
+    if (small && !c->profiling) {
+      long long Bl = (long long)B;
+      const IterArgs* ap = dargs;
+      void* kargs[] = {(void*)&ap, (void*)&small_sp, (void*)&small_sps, (void*)&small_bar, (void*)&Bl};
+      RCG_CUDA(c, cudaLaunchCooperativeKernel((const void*)small_solve_kernel, dim3(small_G), dim3(kThreads), kargs, 0,
+                                              c->stream));
+      c->launches++;
+    } else if (graph_ok) {
       // one graph per (shape, batch size): parameters are all device-resident
       char key[256];
       snprintf(key, sizeof(key), "%p|%lld|%d|%d|%d|%d|%zu|%zu|%d|%d|%lld|%d|%d", (void*)pre, (long long)n,

@@ -16,6 +16,16 @@ from paper_1301_7530_b200.ritz import RitzSpectrum
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True, params=["persistent", "multi_kernel"])
+def solve_loop(request, monkeypatch):
+    """Every reference check runs through both solve loops: the persistent
+    cooperative kernel (small operators, the default here) and the per-phase
+    kernel sequence (RCG_SMALL_N=0)."""
+    if request.param == "multi_kernel":
+        monkeypatch.setenv("RCG_SMALL_N", "0")
+    return request.param
+
+
 def spd(n, rng, cond=100.0):
     return rcg.SparseSpdMatrix.from_dense(problems.random_spd(n, rng, cond), keep_zeros=True)
 

@@ -12,7 +12,7 @@ for A, _ in dev:
     A.device_csr()
 cfg = rcg.SolveConfig(tol=1e-8, max_iters=2000)
 strat = rcg.RecycleStrategy("srks", epsilon=1e-10, nc_limit=21)
-for k in range(4):
+for k in range(8):
     torch.cuda.synchronize(); t = time.perf_counter()
     rep = rcg.run_sequence(iter(dev), rcg.Preconditioner.jacobi, strat, cfg)
     torch.cuda.synchronize(); dt = time.perf_counter() - t
