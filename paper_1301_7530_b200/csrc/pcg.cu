@@ -1445,7 +1445,9 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   const int64_t small_n = env_int("RCG_SMALL_N", 65536);   // read per solve (tests switch paths)
   const bool small = !H && n <= small_n && n <= (int64_t)c->num_sms * SMALL_ROWS && n_c <= NC_INLINE && !store &&
                      !zcap && !A->row_offsets_64 && n > 0;
-  const int small_G = small ? c->num_sms : 0;
+  // one CTA per SM, or fewer when RCG_SMALL_G says so (rows per CTA <= SMALL_ROWS)
+  const int small_G = !small ? 0 : (int)std::min<int64_t>(c->num_sms, std::max<int64_t>(
+      ceil_div(n, (int64_t)SMALL_ROWS), env_int("RCG_SMALL_G", c->num_sms)));
   auto ensure_sums = [&](void) -> int {
     const int64_t need = 8 + n_c + 1 + 2 * reo_cols() + 8;
     if (gSum.cols < need) {
