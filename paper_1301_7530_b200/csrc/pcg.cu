@@ -1442,7 +1442,9 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
 
   auto reo_cols = [&]() { return gAW.cols; };
   // persistent cooperative solve loop for small operators (small_solve_kernel)
-  const int64_t small_n = env_int("RCG_SMALL_N", 65536);   // read per solve (tests switch paths)
+  // crossover (tools/small_threshold.py): persistent wins by 34 % at n = 16 k, 15 % at 33 k,
+  // loses by 6 % at 65 k
+  const int64_t small_n = env_int("RCG_SMALL_N", 49152);   // read per solve (tests switch paths)
   const bool small = !H && n <= small_n && n <= (int64_t)c->num_sms * SMALL_ROWS && n_c <= NC_INLINE && !store &&
                      !zcap && !A->row_offsets_64 && n > 0;
   // one CTA per SM, or fewer when RCG_SMALL_G says so (rows per CTA <= SMALL_ROWS)
