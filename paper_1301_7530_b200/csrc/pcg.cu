@@ -1442,8 +1442,8 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
 
   auto reo_cols = [&]() { return gAW.cols; };
   // persistent cooperative solve loop for small operators (small_solve_kernel)
-  // crossover (tools/small_threshold.py): persistent wins by 34 % at n = 16 k, 15 % at 33 k,
-  // loses by 6 % at 65 k
+  // crossover (tools/small_threshold.py, 3-system sequences): persistent 26.7 vs 38.5 ms
+  // at n = 16 k, 51 vs 60 ms at 33 k, 129 vs 121 ms at 65 k
   const int64_t small_n = env_int("RCG_SMALL_N", 49152);   // read per solve (tests switch paths)
   const bool small = !H && n <= small_n && n <= (int64_t)c->num_sms * SMALL_ROWS && n_c <= NC_INLINE && !store &&
                      !zcap && !A->row_offsets_64 && n > 0;
