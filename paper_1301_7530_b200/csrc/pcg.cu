@@ -1658,7 +1658,9 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   cudaEventRecord(ev0, c->stream);
   SolveState* hst = (SolveState*)c->pinned;
   int64_t it = 0;
-  int64_t batch = cfg->batch > 0 ? cfg->batch : 4;
+  // the persistent loop stops by itself at convergence (blocks return), so it
+  // runs long batches: one host round trip per solve once m is known
+  int64_t batch = cfg->batch > 0 ? cfg->batch : (small ? std::max<int64_t>(64, hint) : 4);
 
   const double jac = inv_diag ? 1.0 : 0.0;
   // algorithmic bytes of the format actually streamed (BSR3: one index per block)
@@ -1809,7 +1811,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     RCG_CUDA(c, cudaStreamSynchronize(c->stream));
     prof_collect(c);
     done = hst->done != 0;
-    batch = std::min<int64_t>(batch * 2, 64);
+    batch = std::min<int64_t>(batch * 2, small ? 4096 : 64);
   }
   cudaEventRecord(ev1, c->stream);
   RCG_CUDA(c, cudaMemcpyAsync(hst, st, sizeof(SolveState), cudaMemcpyDeviceToHost, c->stream));
