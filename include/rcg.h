@@ -49,10 +49,11 @@ typedef struct rcg_trace rcg_trace;
 
 /* CSR operator, full symmetric pattern (SparseSpdMatrix, core.py:34-111).
  * row_offsets is int32 when row_offsets_64 == 0, else int64; col_indices int32.
- * block == 3: the optional bsr_* arrays hold the same operator as 3x3 blocks
- * (built on device by rcg_csr_block3_build) and SpMV streams those instead:
- * one column index per 9 values, ~29% fewer bytes for vector-valued FEM
- * operators such as Q1 elasticity (BASELINE configs 2/3/5). */
+ * Optional SpMV stream copies (the CSR arrays stay valid and are used by the
+ * setup kernels): dia_count > 0 selects the symmetric block-DIA copy (grid
+ * operators); else block == 3 selects the 3x3 block copy in bsr_* (built by
+ * rcg_csr_block3_build, optionally sliced): one column index per 9 values,
+ * ~29% fewer bytes for vector-valued FEM operators (BASELINE configs 2/3/5). */
 typedef struct {
   int64_t n;
   int64_t nnz;
@@ -74,10 +75,12 @@ typedef struct {
   int32_t pad1;
   const int64_t* dia_offsets;       /* [dia_count] upper block-diagonal offsets,
                                        ascending, dia_offsets[0] = 0 (device) */
-  const double* dia_values;         /* dia_count * b*b * 32*ceil(n/b/32): entry
-                                       q = i*b + jj of block (p, p + off_d) at
-                                       ((d*T + p/32)*b*b + q)*32 + p%32,
-                                       T = ceil(n/b/32); 0 = absent */
+  const double* dia_values;         /* dia_count * b*b * 32*ceil(n/b/32)
+                                       doubles; b = 3: entry q = i*b + jj of
+                                       block (p, p + off_d) at
+                                       ((d*T + p/32)*9 + q)*32 + p%32,
+                                       T = ceil(n/96); b = 1: A(p, p + off_d)
+                                       at d*n + p; 0 = absent */
 } rcg_csr;
 
 /* Deflation operator P = I - C G^{-1} (AC)^T, G = C^T A C (DeflationOperator,
