@@ -615,8 +615,8 @@ colreduce_kernel(const IterArgs* __restrict__ ap) {
 // failure decisions from the same partial rows in the same fixed order, so
 // all blocks take identical branches and write identical bits (block 0 writes
 // the trace).  Same arithmetic as K1-K5 (CSR SpMV with sequential row sums,
-// explicitly rounded updates); used only when n <= RCG_SMALL_N, n_c <= 64,
-// no r history, no Krylov cap and no sharding.
+// explicitly rounded updates, r history and capped z history as K2/K3); used
+// when n <= RCG_SMALL_N, n_c <= 64 and not sharded.
 //   sp row b: [0] (w, Aw)  [1] ||r||^2  [2, 2+n_c) AC^T y  [2+n_c] (r, z)
 
 constexpr int SMALL_ROWS = 512;   // max rows per block (n <= 148 * 512)
@@ -709,9 +709,12 @@ small_solve_kernel(const IterArgs* __restrict__ ap, double* sp, int sps, unsigne
       if (a.waw_diag) a.waw_diag[j] = wAw;
     }
     double rr = 0.0;
+    double* __restrict__ rh = a.R.base ? a.R.at(j) : nullptr;      // r history (TRKS)
     for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
+      const double rold = a.r[i];
+      if (rh) rh[i] = rold;
       const double xi = __dadd_rn(a.x[i], __dmul_rn(alpha, w[i]));     // x = x + alpha w
-      const double ri = __dsub_rn(a.r[i], __dmul_rn(alpha, __ldcg(aw + i)));   // r = r - alpha Aw
+      const double ri = __dsub_rn(rold, __dmul_rn(alpha, __ldcg(aw + i)));   // r = r - alpha Aw
       a.x[i] = xi;
       a.r[i] = ri;
       rr += ri * ri;
@@ -1445,8 +1448,8 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   // crossover (tools/small_threshold.py, 3-system sequences): persistent 26.7 vs 38.5 ms
   // at n = 16 k, 51 vs 60 ms at 33 k, 129 vs 121 ms at 65 k
   const int64_t small_n = env_int("RCG_SMALL_N", 49152);   // read per solve (tests switch paths)
-  const bool small = !H && n <= small_n && n <= (int64_t)c->num_sms * SMALL_ROWS && n_c <= NC_INLINE && !store &&
-                     !zcap && !A->row_offsets_64 && n > 0;
+  const bool small = !H && n <= small_n && n <= (int64_t)c->num_sms * SMALL_ROWS && n_c <= NC_INLINE &&
+                     !A->row_offsets_64 && n > 0;
   // one CTA per SM, or fewer when RCG_SMALL_G says so (rows per CTA <= SMALL_ROWS)
   const int small_G = !small ? 0 : (int)std::min<int64_t>(c->num_sms, std::max<int64_t>(
       ceil_div(n, (int64_t)SMALL_ROWS), env_int("RCG_SMALL_G", c->num_sms)));
