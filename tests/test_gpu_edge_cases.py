@@ -12,6 +12,15 @@ from oracle import recycg_oracle as orc
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True, params=["persistent", "multi_kernel"])
+def solve_loop(request, monkeypatch):
+    """Edge cases through both solve loops (persistent cooperative kernel for
+    these small operators by default; the kernel sequence with RCG_SMALL_N=0)."""
+    if request.param == "multi_kernel":
+        monkeypatch.setenv("RCG_SMALL_N", "0")
+    return request.param
+
+
 def _spd(n, rng, cond=100.0):
     return rcg.SparseSpdMatrix.from_dense(problems.random_spd(n, rng, cond), keep_zeros=True)
 
