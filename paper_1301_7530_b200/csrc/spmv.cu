@@ -527,6 +527,182 @@ __global__ void __launch_bounds__(kThreads, B == 3 ? RCG_DIA3_MINB : RCG_DIA1_MI
     spmv_epilogue<1>(d0, d1, sa->part, sa->counter, sa->out);
 }
 
+// 3x3 block-DIA with the UPPER blocks staged by TMA (RCG_DIA3_TMA=1).  In the
+// tiled layout the 9 x 32 values of one (diagonal d, 32-block-row tile) are a
+// contiguous 2,304-B run, so lane 0 of each warp streams its tiles' upper runs
+// with cp.async.bulk into a per-warp ring of S stages (mbarrier complete_tx)
+// while the warp computes the lower blocks (U_d(p - o), mostly L2 hits) from
+// registers.  The HBM bytes in flight then sit in shared memory, not in
+// registers.  Per row the FMA order is dia_body's (lower d = nd-1..1, then
+// d = 0..nd-1; jj ascending inside a block), so y is bitwise the same.
+#ifndef RCG_DIA3T_S
+#define RCG_DIA3T_S 4
+#endif
+#ifndef RCG_DIA3T_KU
+#define RCG_DIA3T_KU 7
+#endif
+constexpr int kDiaChunk = 9 * 32;   // doubles per (d, tile) run
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void tma_chunk(double* dst, const double* src, uint64_t* bar) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(kDiaChunk * 8) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(kDiaChunk * 8), "r"(b)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(b), "r"(parity)
+        : "memory");
+  }
+}
+
+template <int ND>
+__global__ void __launch_bounds__(kThreads, RCG_DIA3_MINB) dia3t_kernel_ind(const SpmvArgs* __restrict__ sa) {
+  // S stages per warp, from the dynamic shared memory size (RCG_DIA3T_S)
+  unsigned dyn;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+  const int S = (int)(dyn / (kWarps * kDiaChunk * 8));
+  extern __shared__ __align__(128) double ring[];   // [kWarps][S][kDiaChunk]
+  __shared__ __align__(8) uint64_t bars[kWarps][8];
+  __shared__ int64_t so[DIA_MAX];
+  pdl_wait();
+  const int nd = ND > 0 ? ND : sa->dia_nd;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0)
+    for (int s = 0; s < S; ++s) mbar_init(&bars[wid][s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  dia_load_offsets(nd, sa->dia_offsets, so);   // includes __syncthreads
+  const SolveState* st = sa->st;
+  double d0 = 0.0;
+  if (st->done) return;
+  const long long j = st->j;
+  const double* __restrict__ x = sa->xs.at(j);
+  double* __restrict__ y = sa->ys.at(j);
+  const double* __restrict__ U = sa->dia_values;
+  const int64_t nbr = sa->n / 3, T = (nbr + 31) >> 5;
+  const int64_t tile0 = (int64_t)blockIdx.x * kWarps + wid, tstride = (int64_t)gridDim.x * kWarps;
+  double* myring = ring + (size_t)wid * S * kDiaChunk;
+  // chunk c of this warp's stream: tile tile0 + (c / nd) * tstride, diagonal c % nd
+  auto issue = [&](int64_t c) {
+    const int64_t t = tile0 + (c / nd) * tstride;
+    if (t < T) {
+      const int d = (int)(c % nd);
+      tma_chunk(myring + (c % S) * kDiaChunk, U + ((int64_t)d * T + t) * kDiaChunk, &bars[wid][c % S]);
+    }
+  };
+  if (lane == 0)
+    for (int c = 0; c < S; ++c) issue(c);
+  constexpr int K = RCG_DIA3_K;
+  int64_t c = 0;   // next chunk to consume
+  for (int64_t t = tile0; t < T; t += tstride) {
+    const int64_t pw = t * 32;
+    const bool act = pw + lane < nbr;
+    const int64_t p = act ? pw + lane : nbr - 1;
+    double acc[3] = {0.0, 0.0, 0.0};
+    // lower blocks d = nd-1 .. 1 through registers (as dia_body)
+#pragma unroll(ND > 0 ? (ND - 1 + K - 1) / K : 1)
+    for (int t0 = 0; t0 < nd - 1; t0 += K) {
+      double v[K][9], xv[K][3];
+      bool ok[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int tt = t0 + k;
+        const int d = tt < nd - 1 ? nd - 1 - tt : 1;
+        const int64_t o = so[d];
+        ok[k] = tt < nd - 1 && p >= o;
+        const int64_t ub = ok[k] ? p - o : 0;
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj) xv[k][jj] = __ldg(x + 3 * ub + jj);
+        const double* __restrict__ u = U + dia_at(d, 0, ub, nbr, 9);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) v[k][q] = __ldg(u + q * 32);
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int jj = 0; jj < 3; ++jj) acc[i] = fma(ok[k] ? v[k][jj * 3 + i] : 0.0, ok[k] ? xv[k][jj] : 0.0, acc[i]);
+    }
+    // diagonal and upper blocks d = 0 .. nd-1 from the TMA ring; the x loads
+    // of KU terms are issued together (L2 latency), then each term waits for
+    // its run, reads it and hands the stage back to the next run
+    constexpr int KU = RCG_DIA3T_KU;
+    double xd[3];
+#pragma unroll(ND > 0 ? (ND + KU - 1) / KU : 1)
+    for (int u0 = 0; u0 < nd; u0 += KU) {
+      double xv[KU][3];
+      bool ok[KU];
+#pragma unroll
+      for (int k = 0; k < KU; ++k) {
+        const int d = u0 + k < nd ? u0 + k : 0;
+        const int64_t o = so[d];
+        ok[k] = u0 + k < nd && p + o < nbr;
+        const int64_t xb = ok[k] ? p + o : p;
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj) xv[k][jj] = __ldg(x + 3 * xb + jj);
+      }
+      if (u0 == 0) {
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj) xd[jj] = xv[0][jj];
+      }
+#pragma unroll
+      for (int k = 0; k < KU; ++k) {
+        if (u0 + k >= nd) break;
+        mbar_wait(&bars[wid][c % S], (unsigned)((c / S) & 1));
+        const double* sv = myring + (c % S) * kDiaChunk + lane;
+        double v[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) v[q] = sv[q * 32];
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(c + S);
+        }
+        ++c;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int jj = 0; jj < 3; ++jj)
+            acc[i] = fma(ok[k] ? v[i * 3 + jj] : 0.0, ok[k] ? xv[k][jj] : 0.0, acc[i]);
+      }
+    }
+    if (!act) continue;
+    const int64_t r = 3 * p;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      d0 += xd[i] * acc[i];
+      y[r + i] = acc[i];
+    }
+  }
+  spmv_epilogue<1>(d0, 0.0, sa->part, sa->counter, sa->out);
+}
+
+static bool dia3_tma() {
+  static const bool on = [] {
+    const char* e = getenv("RCG_DIA3_TMA");
+    return e && atoi(e) != 0;
+  }();
+  return on;
+}
+static size_t dia3t_smem() {
+  static const int S = [] {
+    const char* e = getenv("RCG_DIA3T_S");
+    return e ? std::min(8, std::max(2, atoi(e))) : RCG_DIA3T_S;
+  }();
+  return sizeof(double) * (size_t)kWarps * S * kDiaChunk;
+}
+
 // Exactly one wave of resident CTAs of the kernel actually launched (its own
 // occupancy: the variants use 32-100 registers): a grid-stride sweep then
 // moves through the rows as one front, so the lower blocks U_d(p - o) and the
@@ -903,6 +1079,13 @@ static int dia_grid_for(Ctx* c, const rcg_csr* A, int mode, bool ind) {
   const int64_t nbr = A->n / A->dia_block;
   const int nd = A->dia_count;
   const void* k;
+  if (A->dia_block == 3 && ind && dia3_tma() && RCG_DIA_TILED) {
+    k = nd == 14 ? (const void*)dia3t_kernel_ind<14> : (const void*)dia3t_kernel_ind<0>;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, dia3t_smem()) != cudaSuccess || occ < 1)
+      occ = 1;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nbr, kThreads), (int64_t)c->num_sms * occ));
+  }
   if (A->dia_block == 3) {
     if (ind) k = nd == 14 ? (const void*)dia_kernel_ind<3, 14> : (const void*)dia_kernel_ind<3, 0>;
     else if (nd == 14) k = mode == 0 ? (const void*)dia_kernel<3, 0, 14> : mode == 1 ? (const void*)dia_kernel<3, 1, 14> : (const void*)dia_kernel<3, 2, 14>;
@@ -986,10 +1169,22 @@ int launch_spmv_ind(Ctx* c, const rcg_csr* A, const SpmvArgs* dargs) {
   // one solve-loop kernel per stream format, launched with PDL (launch_k)
   void (*k)(const SpmvArgs*) = nullptr;
   int grid = 1;
+  size_t smem = 0;
   if (is_dia(A)) {
-    grid = dia_grid_for(c, A, 1, true);
     const int nd = A->dia_count;
-    if (A->dia_block == 3) k = nd == 14 ? dia_kernel_ind<3, 14> : dia_kernel_ind<3, 0>;
+    if (A->dia_block == 3 && dia3_tma() && RCG_DIA_TILED) {
+      k = nd == 14 ? dia3t_kernel_ind<14> : dia3t_kernel_ind<0>;
+      smem = dia3t_smem();
+      static bool attr14 = false, attr0 = false;
+      bool& done_attr = nd == 14 ? attr14 : attr0;
+      if (!done_attr) {
+        RCG_CUDA(c, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        done_attr = true;
+      }
+    }
+    grid = dia_grid_for(c, A, 1, true);
+    if (k) {
+    } else if (A->dia_block == 3) k = nd == 14 ? dia_kernel_ind<3, 14> : dia_kernel_ind<3, 0>;
     else k = nd == 3 ? dia_kernel_ind<1, 3> : (nd == 4 ? dia_kernel_ind<1, 4> : dia_kernel_ind<1, 0>);
   } else if (is_sell3(A)) {
     grid = sell3_grid(c, A->n / 3);
@@ -1007,7 +1202,7 @@ int launch_spmv_ind(Ctx* c, const rcg_csr* A, const SpmvArgs* dargs) {
       k = V == 1 ? spmv_kernel_ind<int32_t, 1> : V == 2 ? spmv_kernel_ind<int32_t, 2> : V == 4 ? spmv_kernel_ind<int32_t, 4>
         : V == 8 ? spmv_kernel_ind<int32_t, 8> : V == 16 ? spmv_kernel_ind<int32_t, 16> : spmv_kernel_ind<int32_t, 32>;
   }
-  RCG_CUDA(c, launch_k(k, dim3(grid), dim3(kThreads), 0, c->stream, dargs));
+  RCG_CUDA(c, launch_k(k, dim3(grid), dim3(kThreads), smem, c->stream, dargs));
   c->launches++;
   return RCG_OK;
 }
