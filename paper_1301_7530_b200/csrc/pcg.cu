@@ -647,9 +647,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int& ge
 // fixed-order sum over the G block rows of column `col` (stride `ld`), same
 // bits in every block: lanes stride the rows, then a fixed shuffle tree
 __device__ __forceinline__ double grid_sum_col(const double* part, int ld, int col, int G) {
-  double s = 0.0;
-  for (int b = threadIdx.x & 31; b < G; b += 32) s += __ldcg(part + (size_t)b * ld + col);
-  return warp_sum(s);
+  return warp_sum(lane_strided_sum(part + col, G, ld, threadIdx.x & 31));
 }
 
 __global__ void __launch_bounds__(kThreads, 1)

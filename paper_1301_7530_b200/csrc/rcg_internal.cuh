@@ -186,6 +186,24 @@ __device__ __forceinline__ bool arrive_last(unsigned int* counter) {
   return last;
 }
 
+// sum of p[b * stride] over b = lane, lane + 32, ... < nb, added in exactly
+// that order (so the same bits as the plain loop); the loads of 8 steps are
+// issued before their adds: in the last-block tails below a plain loop waits
+// one L2 round trip per step
+__device__ __forceinline__ double lane_strided_sum(const double* p, int nb, int64_t stride, int lane) {
+  double s = 0.0;
+  int b = lane;
+  for (; b + 32 * 7 < nb; b += 32 * 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcg(p + (size_t)(b + 32 * u) * stride);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
+  }
+  for (; b < nb; b += 32) s += __ldcg(p + (size_t)b * stride);
+  return s;
+}
+
 // Deterministic reduction of part[b*K + k] over b < nb for k < K into out[k]
 // by one block of NT threads: warps own k's; lanes stride over blocks in a
 // fixed order then a fixed shuffle tree.
@@ -193,8 +211,7 @@ template <int NT>
 __device__ void reduce_partials(const double* part, int nb, int K, double* out) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int k = wid; k < K; k += NT / 32) {
-    double s = 0.0;
-    for (int b = lane; b < nb; b += 32) s += __ldcg(part + (size_t)b * K + k);
+    double s = lane_strided_sum(part + k, nb, K, lane);
     s = warp_sum(s);
     if (lane == 0) out[k] = s;
   }
@@ -205,8 +222,7 @@ template <int NT>
 __device__ void reduce_partials_strided(const double* part, int nb, int stride, int count, double* out) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int k = wid; k < count; k += NT / 32) {
-    double s = 0.0;
-    for (int b = lane; b < nb; b += 32) s += __ldcg(part + (size_t)b * stride + k);
+    double s = lane_strided_sum(part + k, nb, stride, lane);
     s = warp_sum(s);
     if (lane == 0) out[k] = s;
   }

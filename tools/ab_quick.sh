@@ -1,0 +1,4 @@
+# quick config-2 bench on 2 systems: per-kernel seconds and GB/s, iterations
+for i in 1 2; do
+  timeout 200 python bench.py --systems 2 --steps 1 --warmup 1 --no-cpu --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); k=d['roofline']['all_kernels']; print(round(d['value'],1), d['iterations_per_system'], {n:(round(v['seconds'],4), round(v['GBps'])) for n,v in k.items() if v['launches']})"
+done
