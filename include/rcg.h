@@ -330,6 +330,15 @@ int rcg_select_converged(rcg_ctx* ctx, const double* cur, const double* prev, in
 int rcg_ritz_select(rcg_ctx* ctx, const double* alphas, const double* betas, int64_t m,
                     double epsilon, double* d_work, double* e_work,
                     double* values, double* prev, uint8_t* mask);
+/* Cluster filter (replaces ritz.py:141-183, cluster_filter): the central
+ * dense cluster of the m Ritz values (device array, descending) as the value
+ * index range [range_host[0], range_host[1]]; the filter keeps the indices
+ * outside it.  Same scores and tie order as the reference (best three-segment
+ * constant fit of the gaps; ties -> larger cluster, smaller gap level, smaller
+ * start).  m < max(2, min_cluster): empty range {m, m-1}.  min_cluster < 1:
+ * RCG_ERR_CONTRACT.  Synchronizes. */
+int rcg_cluster_filter(rcg_ctx* ctx, const double* values, int64_t m, int64_t min_cluster,
+                       int64_t* range_host);
 /* Ritz vectors y_i = V q_{idx_i} with V = [(-1)^j z_j / sqrt(rz_j)] (ritz.py:
  * 81-100), scaled by 1/sqrt(|theta_i|) when scale_by_theta != 0 (the SRKS
  * block, recycle.py:151), written to Y (n x k, ld ldy).  Forms only the k

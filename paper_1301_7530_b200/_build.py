@@ -31,15 +31,31 @@ def needs_rebuild():
 
 
 def build(force=False, verbose=True, extra=()):
+    """One nvcc per translation unit, in parallel (objects under build/), then
+    one shared-library link."""
     if not force and not needs_rebuild():
         return LIB
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-v" if os.environ.get("RCG_PTXAS_VERBOSE") else "-O3",
-           "-I", str(PKG.parent / "include"), "-o", str(LIB) + ".tmp",
-           *[str(CSRC / s) for s in SOURCES], "-ldl", *extra]
+    from concurrent.futures import ThreadPoolExecutor
+    obj_dir = PKG.parent / "build" / "obj"
+    obj_dir.mkdir(parents=True, exist_ok=True)
+    common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+              "-Xptxas", "-v" if os.environ.get("RCG_PTXAS_VERBOSE") else "-O3",
+              "-I", str(PKG.parent / "include"), *extra]
+
+    def compile_one(src):
+        obj = obj_dir / (Path(src).stem + ".o")
+        cmd = [*common, "-c", str(CSRC / src), "-o", str(obj)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        return str(obj)
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    link = [nvcc(), *ARCH, "-shared", "-o", str(LIB) + ".tmp", *objs, "-ldl"]
     if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+        print(" ".join(link), file=sys.stderr)
+    subprocess.run(link, check=True)
     os.replace(str(LIB) + ".tmp", LIB)
     return LIB
 

@@ -124,6 +124,7 @@ SIGNATURES = {
     "rcg_tridiag_eigvals": (C.c_int, [_vp, _vp, _vp, _i64, _vp]),
     "rcg_tridiag_eigvecs": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _vp, _i64, _vp]),
     "rcg_select_converged": (C.c_int, [_vp, _vp, _vp, _i64, _d, _vp]),
+    "rcg_cluster_filter": (C.c_int, [_vp, _vp, _i64, _i64, c_int64_p]),
     "rcg_ritz_select": (C.c_int, [_vp, _vp, _vp, _i64, _d, _vp, _vp, _vp, _vp, _vp]),
     "rcg_ritz_vectors": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _i64, _i32, _vp, _i64]),
     "rcg_column_norms": (C.c_int, [_vp, _i64, _i64, _vp, _i64, _vp]),

@@ -209,11 +209,12 @@ static cudaEvent_t pool_get(Ctx* c) {
   return e;
 }
 
-void prof_begin(Ctx* c, int kclass, double bytes) {
+void prof_begin(Ctx* c, int kclass, double bytes, int64_t jj) {
   if (!c->profiling) return;
   Ctx::Pending p;
   p.kclass = kclass;
   p.bytes = bytes;
+  p.jj = jj;
   p.a = pool_get(c);
   p.b = pool_get(c);
   cudaEventRecord(p.a, c->stream);
@@ -225,10 +226,14 @@ void prof_end(Ctx* c) {
   cudaEventRecord(c->pending.back().b, c->stream);
 }
 
-void prof_collect(Ctx* c) {
+void prof_collect(Ctx* c, int64_t stop_j) {
   for (auto& p : c->pending) {
     float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+    const bool late = p.kclass == RCG_K_PRECOND || p.kclass == RCG_K_COLREDUCE || p.kclass == RCG_K_WUPDATE;
+    const bool noop = stop_j >= 0 && p.jj >= 0 && (p.jj > stop_j || (p.jj == stop_j && late));
+    if (noop) {
+      // queued after the solve stopped: returned at the done flag, no bytes moved
+    } else if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
       c->stats[p.kclass].launches += 1;
       c->stats[p.kclass].seconds += ms * 1e-3;
       c->stats[p.kclass].bytes += p.bytes;
@@ -300,7 +305,7 @@ extern "C" void rcg_ctx_destroy(rcg_ctx* c) {
   if (!c) return;
   cudaStreamSynchronize(c->stream);
   comm_free(c);
-  for (auto& g : c->graphs) cudaGraphExecDestroy(g.second.first);
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.second.exec);
   if (c->dargs) cudaFree(c->dargs);
   if (c->capture_stream) cudaStreamDestroy(c->capture_stream);
   if (c->scratch) {

@@ -80,6 +80,7 @@ struct IterArgs {
   SolveState* st;
   int reorth;
   int rows_per_block;      // K3 row tile
+  int s_smem;              // K3 stages the coarse solution s in smem (0: reads s_ext, n_c too large)
   int rows_per_block_upd;  // K2 row tile (smaller: its AC^T y GEMV-T has few columns)
   int rows_per_block_actr; // K2b row tile (long: ~4 CTAs/SM over all column groups)
   int nb_pre;              // K3 row tiles (partial rows in part_reo / part_z)
@@ -482,8 +483,8 @@ precond_kernel(const IterArgs* __restrict__ ap, int init) {
   const int RT = a.reorth ? R : 0;
   double* ztile = dyn;            // R (reorth only)
   double* wtile = dyn + RT;       // R (reorth only)
-  double* s = dyn + 2 * RT;       // n_c
-  if (a.n_c) {
+  double* s = a.s_smem ? dyn + 2 * RT : a.s_ext;   // n_c (global when it does not fit in smem)
+  if (a.n_c && a.s_smem) {
     if (a.n_c <= NC_INLINE) {
       // s_i = sum_k Ginv[i,k] u_k, fixed order (every CTA computes the same s)
       const double* u = a.sums + 2;
@@ -1109,18 +1110,28 @@ gemv_t_kernel(int64_t n, int64_t k, const double* __restrict__ X, int64_t ldx, c
   if (arrive_last(counter)) reduce_partials<kThreads>(part, gridDim.x, (int)k, out);
 }
 
+// s = G^{-1} u, one thread per row with a sequential (fixed-order) sum
+__global__ void __launch_bounds__(kThreads)
+coarse_s_kernel(int64_t n_c, const double* __restrict__ Ginv, const double* __restrict__ u, double* s) {
+  const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (i >= n_c) return;
+  const double* g = Ginv + i * n_c;
+  double acc = 0.0;
+  for (int64_t kk = 0; kk < n_c; ++kk) acc += g[kk] * u[kk];
+  s[i] = acc;
+}
+
+// out = base - X s (or X s): s staged in smem when it fits, else read from
+// global memory (L2-resident, uniform across the warp)
 __global__ void __launch_bounds__(kThreads)
 coarse_combine_kernel(int64_t n, int64_t n_c, const double* __restrict__ X, int64_t ldx,
-                      const double* __restrict__ Ginv, const double* __restrict__ u,
-                      const double* __restrict__ base, double* out) {
-  extern __shared__ double s[];
-  for (int64_t i = threadIdx.x; i < n_c; i += kThreads) {
-    const double* g = Ginv + i * n_c;
-    double acc = 0.0;
-    for (int64_t kk = 0; kk < n_c; ++kk) acc += g[kk] * u[kk];
-    s[i] = acc;
+                      const double* __restrict__ s_glob, int stage, const double* __restrict__ base, double* out) {
+  extern __shared__ double s_sm[];
+  if (stage) {
+    for (int64_t i = threadIdx.x; i < n_c; i += kThreads) s_sm[i] = s_glob[i];
+    __syncthreads();
   }
-  __syncthreads();
+  const double* s = stage ? s_sm : s_glob;
   for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
     double cs = 0.0;
     for (int64_t c = 0; c < n_c; ++c) cs += X[c * ldx + i] * s[c];
@@ -1182,13 +1193,21 @@ int gemv_t(Ctx* c, int64_t n, int64_t k, const double* X, int64_t ldx, const dou
 }
 
 int coarse_combine(Ctx* c, const rcg_deflation* D, const double* u, const double* base, double* out) {
-  const size_t smem = sizeof(double) * (size_t)std::max<int64_t>(D->n_c, 1);
-  if (smem > 48 * 1024)
-    RCG_CUDA(c, cudaFuncSetAttribute(coarse_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-  coarse_combine_kernel<<<elementwise_grid(c, D->n), kThreads, smem, c->stream>>>(D->n, D->n_c, D->C, D->ldc,
-                                                                                  D->Ginv, u, base, out);
-  RCG_LAUNCH_CHECK(c);
+  const int64_t n_c = std::max<int64_t>(D->n_c, 1);
+  double* sv = nullptr;
+  RCG_CUDA(c, cudaMallocAsync((void**)&sv, sizeof(double) * (size_t)n_c, c->stream));
+  coarse_s_kernel<<<(unsigned)ceil_div(n_c, (int64_t)kThreads), kThreads, 0, c->stream>>>(D->n_c, D->Ginv, u, sv);
+  cudaError_t e = cudaGetLastError();
+  const size_t smem = sizeof(double) * (size_t)n_c;
+  const int stage = smem <= 48 * 1024 ? 1 : 0;
+  if (e == cudaSuccess) {
+    coarse_combine_kernel<<<elementwise_grid(c, D->n), kThreads, stage ? smem : 0, c->stream>>>(
+        D->n, D->n_c, D->C, D->ldc, sv, stage, base, out);
+    e = cudaGetLastError();
+  }
+  c->launches += 2;
+  cudaFreeAsync(sv, c->stream);
+  if (e != cudaSuccess) return set_error(c, RCG_ERR_CUDA, "coarse combine: %s", cudaGetErrorString(e));
   return RCG_OK;
 }
 
@@ -1330,6 +1349,22 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     rcg_trace_free(T);
     return rc;
   };
+  // after this point every error path returns the solve's pooled buffers,
+  // histories and trace (fail) instead of leaking them
+#define RCG_CUDA_F(call)                                                                  \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(set_error(c, RCG_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__)); \
+  } while (0)
+#define RCG_LAUNCH_CHECK_F()                                                              \
+  do {                                                                                    \
+    c->launches++;                                                                        \
+    cudaError_t e_ = cudaGetLastError();                                                  \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(set_error(c, RCG_ERR_CUDA, "launch: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, __LINE__)); \
+  } while (0)
+
   auto alloc = [&](size_t bytes, void** p) -> int {
     bytes = std::max<size_t>(bytes, 256);
     *p = c->pool->get(bytes);
@@ -1412,10 +1447,10 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   if ((rc = alloc(sizeof(double) * (n_c + 1), (void**)&s_ext))) return fail(rc);
   const size_t n_counters = 16 + (size_t)wu_grid;
   if ((rc = alloc(sizeof(unsigned int) * n_counters, (void**)&counters))) return fail(rc);
-  RCG_CUDA(c, cudaMemsetAsync(counters, 0, sizeof(unsigned int) * n_counters, c->stream));
+  RCG_CUDA_F(cudaMemsetAsync(counters, 0, sizeof(unsigned int) * n_counters, c->stream));
   double* part_wu = nullptr;
   if (wu_split > 1 && (rc = alloc(sizeof(double) * (size_t)wu_split * n, (void**)&part_wu))) return fail(rc);
-  RCG_CUDA(c, cudaMemsetAsync(hist, 0, sizeof(double) * 5 * nh, c->stream));
+  RCG_CUDA_F(cudaMemsetAsync(hist, 0, sizeof(double) * 5 * nh, c->stream));
   double* alphas = hist;
   double* betas = hist + nh;
   double* rzh = hist + 2 * nh;
@@ -1492,8 +1527,19 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   if (small) {
     if ((rc = alloc(sizeof(double) * (size_t)small_G * small_sps + 256, (void**)&small_sp))) return fail(rc);
     small_bar = (unsigned int*)(small_sp + (size_t)small_G * small_sps);
-    RCG_CUDA(c, cudaMemsetAsync(small_bar, 0, 64, c->stream));
+    RCG_CUDA_F(cudaMemsetAsync(small_bar, 0, 64, c->stream));
   }
+  const int64_t nc_bucket = ((n_c + 1 + 63) / 64) * 64;
+  const size_t smem_upd = sizeof(double) * (n_c ? Ru : 1);
+  // z / w_j tiles only when reorthogonalizing (they feed the AW GEMV-T); the
+  // coarse solution s joins them in smem while it fits (a TRKS basis can grow
+  // past the opt-in limit: then K3 reads s from s_ext, L2-resident)
+  const size_t smem_tiles = sizeof(double) * (reorth ? 2 * (size_t)R : 0);
+  const bool s_smem = n_c <= NC_INLINE || smem_tiles + sizeof(double) * nc_bucket <= c->smem_optin;
+  const size_t smem_pre = smem_tiles + (s_smem ? sizeof(double) * nc_bucket : 0);
+  if (smem_pre > c->smem_optin)
+    return fail(set_error(c, RCG_ERR_CONTRACT, "K3 tile of %d rows needs %zu B of shared memory (limit %zu)", R,
+                          smem_pre, c->smem_optin));
   IterArgs a{};
   auto refresh = [&]() {
     a.n = n;
@@ -1527,6 +1573,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     a.st = st;
     a.reorth = reorth ? 1 : 0;
     a.rows_per_block = R;
+    a.s_smem = s_smem ? 1 : 0;
     a.rows_per_block_upd = Ru;
     a.rows_per_block_actr = Ra;
     a.nb_pre = nb;
@@ -1543,15 +1590,11 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     // before return, so the host struct may change right after)
     return cudaMemcpyAsync(dargs, &a, sizeof(IterArgs), cudaMemcpyHostToDevice, c->stream);
   };
-  RCG_CUDA(c, refresh());
+  RCG_CUDA_F(refresh());
 
   // dynamic smem sized by n_c bucket so graphs are reusable across the
   // systems of a sequence (n_c changes from system to system)
-  const int64_t nc_bucket = ((n_c + 1 + 63) / 64) * 64;
-  const size_t smem_upd = sizeof(double) * (n_c ? Ru : 1);
-  // z / w_j tiles only when reorthogonalizing (they feed the AW GEMV-T)
-  const size_t smem_pre = sizeof(double) * ((reorth ? 2 * (size_t)R : 0) + nc_bucket);
-  RCG_CUDA(c, cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  RCG_CUDA_F(cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(smem_upd, 1024)));
   static const int pre_cg = env_int("RCG_PRE_CG", 8);
   static const bool pre_pf = env_int("RCG_PF", 0) != 0;
@@ -1559,7 +1602,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
              : (pre_cg == 4 ? precond_kernel<4, false, true>
                             : (pre_cg == 2 ? precond_kernel<2, false, true>
                                            : (pre_pf ? precond_kernel<8, true, true> : precond_kernel<8, false, true>)));
-  RCG_CUDA(c, cudaFuncSetAttribute(pre, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  RCG_CUDA_F(cudaFuncSetAttribute(pre, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(smem_pre, 1024)));
 
   // ---- initial guess and residual (solver.py:208-219) ----
@@ -1567,7 +1610,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
   hs.j = 0;
   hs.iterations = 0;
   hs.done = 0;
-  RCG_CUDA(c, cudaMemcpyAsync(st, &hs, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
+  RCG_CUDA_F(cudaMemcpyAsync(st, &hs, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
   double* norms2 = nullptr;  // ||r0||^2, ||b||^2
   if ((rc = alloc(sizeof(double) * 16, (void**)&norms2))) return fail(rc);
   if (n_c) {
@@ -1580,23 +1623,23 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     if ((rc = halo_exchange(c, H, colsel(xext), nullptr, xext))) return fail(rc);
     if ((rc = launch_spmv(c, A, 2, colsel(xext), colsel(r), b, nullptr, part_spmv, counters + 0, norms2)))
       return fail(rc);
-    RCG_CUDA(c, cudaMemcpyAsync(x, xext, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+    RCG_CUDA_F(cudaMemcpyAsync(x, xext, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
   } else {
     copy_norms_kernel<<<elementwise_grid(c, n), kThreads, 0, c->stream>>>(n, b, r, x, part_spmv, counters + 0,
                                                                         norms2);
-    RCG_LAUNCH_CHECK(c);
+    RCG_LAUNCH_CHECK_F();
   }
   if ((rc = allreduce_h(H, c, norms2, 2))) return fail(rc);
   double hn[2] = {0.0, 0.0};
-  RCG_CUDA(c, cudaMemcpyAsync(hn, norms2, sizeof(hn), cudaMemcpyDeviceToHost, c->stream));
-  RCG_CUDA(c, cudaStreamSynchronize(c->stream));
+  RCG_CUDA_F(cudaMemcpyAsync(hn, norms2, sizeof(hn), cudaMemcpyDeviceToHost, c->stream));
+  RCG_CUDA_F(cudaStreamSynchronize(c->stream));
   const double r0 = std::sqrt(hn[0]);
   const double bn = std::sqrt(hn[1]);
   T->view.n = n;
   T->view.r0_norm = r0;
   T->view.b_norm = bn;
   T->view.ld = ld;
-  RCG_CUDA(c, cudaMemcpyAsync(rnorms, &r0, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  RCG_CUDA_F(cudaMemcpyAsync(rnorms, &r0, sizeof(double), cudaMemcpyHostToDevice, c->stream));
 
   auto finish_view = [&](void) {
     T->view.alphas = alphas;
@@ -1627,7 +1670,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     return RCG_OK;
   }
   hs.tol_abs = cfg->tol * r0;
-  RCG_CUDA(c, cudaMemcpyAsync(st, &hs, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
+  RCG_CUDA_F(cudaMemcpyAsync(st, &hs, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
 
   auto launch_coarse = [&](int check_done) -> int {
     if (n_c > NC_INLINE) {
@@ -1639,18 +1682,18 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
 
   // ---- z0, rz0, w0 (solver.py:221-231) ----
   update_kernel<<<nbu_l, kThreads, 0, c->stream>>>(dargs, 1);
-  RCG_LAUNCH_CHECK(c);
+  RCG_LAUNCH_CHECK_F();
   if (n_c) {
     actr_kernel<<<dim3(nta, (unsigned)ngr), kThreads, 0, c->stream>>>(dargs);
-    RCG_LAUNCH_CHECK(c);
+    RCG_LAUNCH_CHECK_F();
   }
   if ((rc = allreduce_h(H, c, gSum.ptr + 1, (size_t)(1 + n_c)))) return fail(rc);
   if ((rc = launch_coarse(1))) return fail(rc);
   pre<<<nb_l, kThreads, smem_pre, c->stream>>>(dargs, 1);
-  RCG_LAUNCH_CHECK(c);
+  RCG_LAUNCH_CHECK_F();
   if ((rc = allreduce_h(H, c, gSum.ptr + a.rz_off, 1))) return fail(rc);
   init_finish_kernel<<<1, 1, 0, c->stream>>>(dargs);
-  RCG_LAUNCH_CHECK(c);
+  RCG_LAUNCH_CHECK_F();
 
   // ---- the loop (solver.py:241-288), batched ----
   cudaEvent_t ev0, ev1;
@@ -1685,16 +1728,16 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
         if ((rc2 = halo_exchange(c, H, a.W, st, wcol))) return rc2;
       }
       // algorithmic bytes per launch (each operand touched once)
-      if (direct) prof_begin(c, RCG_K_SPMV, bytes_spmv);
+      if (direct) prof_begin(c, RCG_K_SPMV, bytes_spmv, jj);
       if ((rc2 = launch_spmv_ind(c, A, &dargs->spmv))) return rc2;
       if (direct) prof_end(c);
       if ((rc2 = allreduce_h(H, c, gSum.ptr, 1))) return rc2;
-      if (direct) prof_begin(c, RCG_K_UPDATE, 8.0 * nd * (6 + (store ? 1 : 0)));
+      if (direct) prof_begin(c, RCG_K_UPDATE, 8.0 * nd * (6 + (store ? 1 : 0)), jj);
       RCG_CUDA(c, launch_k(update_kernel, dim3(nbu_l), dim3(kThreads), 0, c->stream, (const IterArgs*)dargs, 0));
       c->launches++;
       if (direct) prof_end(c);
       if (n_c) {
-        if (direct) prof_begin(c, RCG_K_ACTR, 8.0 * nd * (1 + jac + n_c));
+        if (direct) prof_begin(c, RCG_K_ACTR, 8.0 * nd * (1 + jac + n_c), jj);
         RCG_CUDA(c, launch_k(actr_kernel, dim3(nta, (unsigned)ngr), dim3(kThreads), 0, c->stream,
                              (const IterArgs*)dargs));
         c->launches++;
@@ -1702,23 +1745,23 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
       }
       if ((rc2 = allreduce_h(H, c, gSum.ptr + 1, (size_t)(1 + n_c)))) return rc2;
       if (n_c > NC_INLINE) {
-        if (direct) prof_begin(c, RCG_K_COARSE, 8.0 * (double)n_c * (double)n_c);
+        if (direct) prof_begin(c, RCG_K_COARSE, 8.0 * (double)n_c * (double)n_c, jj);
         if ((rc2 = launch_coarse(1))) return rc2;
         if (direct) prof_end(c);
       }
-      if (direct) prof_begin(c, RCG_K_PRECOND, 8.0 * nd * (2 + jac + n_c + (reorth ? 1.0 + js : 0.0)));
+      if (direct) prof_begin(c, RCG_K_PRECOND, 8.0 * nd * (2 + jac + n_c + (reorth ? 1.0 + js : 0.0)), jj);
       RCG_CUDA(c, launch_k(pre, dim3(nb_l, pre_split), dim3(kThreads), smem_pre, c->stream, (const IterArgs*)dargs, 0));
       c->launches++;
       if (direct) prof_end(c);
       if (reorth) {
-        if (direct) prof_begin(c, RCG_K_COLREDUCE, 8.0 * 2.0 * js * (nb + 1));
+        if (direct) prof_begin(c, RCG_K_COLREDUCE, 8.0 * 2.0 * js * (nb + 1), jj);
         RCG_CUDA(c, launch_k(colreduce_kernel, dim3(cr_grid), dim3(256), 0, c->stream, (const IterArgs*)dargs));
         c->launches++;
         if (direct) prof_end(c);
       }
       // one packed allreduce: (r, z) and the 2(j+1) reorth dot products
       if ((rc2 = allreduce_h(H, c, gSum.ptr + a.rz_off, (size_t)(1 + (reorth ? 2 * (jj + 1) : 0))))) return rc2;
-      if (direct) prof_begin(c, RCG_K_WUPDATE, 8.0 * nd * (3 + (reorth ? js : 0.0)));
+      if (direct) prof_begin(c, RCG_K_WUPDATE, 8.0 * nd * (3 + (reorth ? js : 0.0)), jj);
       if (!reorth)
         RCG_CUDA(c, launch_k(wupdate_plain_kernel<8>, dim3(wu_plain_grid), dim3(kThreads), 0, c->stream,
                              (const IterArgs*)dargs));
@@ -1757,14 +1800,14 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     }
     if (regrown) {
       if ((rc = ensure_sums())) return fail(rc);
-      RCG_CUDA(c, refresh());
+      RCG_CUDA_F(refresh());
     }
     const bool graph_ok = use_graphs && !c->profiling && !H;
     if (small && !c->profiling) {
       long long Bl = (long long)B;
       const IterArgs* ap = dargs;
       void* kargs[] = {(void*)&ap, (void*)&small_sp, (void*)&small_sps, (void*)&small_bar, (void*)&Bl};
-      RCG_CUDA(c, cudaLaunchCooperativeKernel((const void*)small_solve_kernel, dim3(small_G), dim3(kThreads), kargs, 0,
+      RCG_CUDA_F(cudaLaunchCooperativeKernel((const void*)small_solve_kernel, dim3(small_G), dim3(kThreads), kargs, 0,
                                               c->stream));
       c->launches++;
     } else if (graph_ok) {
@@ -1777,12 +1820,21 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
       cudaGraphExec_t exec = nullptr;
       auto gi = c->graphs.find(key);
       if (gi != c->graphs.end()) {
-        exec = gi->second.first;
+        exec = gi->second.exec;
       } else {
+        // bounded cache: evict the least recently used shape.  Every batch
+        // ends with a stream synchronize, so no cached graph is in flight.
+        if (c->graphs.size() >= Ctx::kMaxGraphs) {
+          auto lru = c->graphs.begin();
+          for (auto g = c->graphs.begin(); g != c->graphs.end(); ++g)
+            if (g->second.last < lru->second.last) lru = g;
+          cudaGraphExecDestroy(lru->second.exec);
+          c->graphs.erase(lru);
+        }
         cudaGraph_t graph = nullptr;
         // capture on a private stream (the caller's may be the legacy default
         // stream, which cannot capture); the graph is launched on c->stream
-        if (!c->capture_stream) RCG_CUDA(c, cudaStreamCreateWithFlags(&c->capture_stream, cudaStreamNonBlocking));
+        if (!c->capture_stream) RCG_CUDA_F(cudaStreamCreateWithFlags(&c->capture_stream, cudaStreamNonBlocking));
         cudaStream_t user_stream = c->stream;
         c->stream = c->capture_stream;
         cudaError_t ce = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
@@ -1799,24 +1851,26 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
         ce = cudaGraphInstantiate(&exec, graph, 0);
         cudaGraphDestroy(graph);
         if (ce != cudaSuccess) return fail(set_error(c, RCG_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ce)));
-        c->graphs[key] = std::make_pair(exec, c->launches - l0);
+        c->graphs[key] = Ctx::GraphEntry{exec, c->launches - l0, 0};
         c->launches = l0;
       }
-      RCG_CUDA(c, cudaGraphLaunch(exec, c->stream));
-      c->launches += c->graphs[key].second;
+      Ctx::GraphEntry& ge = c->graphs[key];
+      ge.last = ++c->graph_tick;
+      RCG_CUDA_F(cudaGraphLaunch(exec, c->stream));
+      c->launches += ge.kernels;
     } else {
       if ((rc = launch_batch(B, it, true))) return fail(rc);
     }
     it += B;
-    RCG_CUDA(c, cudaMemcpyAsync(hst, st, sizeof(SolveState), cudaMemcpyDeviceToHost, c->stream));
-    RCG_CUDA(c, cudaStreamSynchronize(c->stream));
-    prof_collect(c);
+    RCG_CUDA_F(cudaMemcpyAsync(hst, st, sizeof(SolveState), cudaMemcpyDeviceToHost, c->stream));
+    RCG_CUDA_F(cudaStreamSynchronize(c->stream));
     done = hst->done != 0;
+    prof_collect(c, done ? (hst->converged ? hst->iterations - 1 : hst->j) : -1);
     batch = std::min<int64_t>(batch * 2, small ? 4096 : 64);
   }
   cudaEventRecord(ev1, c->stream);
-  RCG_CUDA(c, cudaMemcpyAsync(hst, st, sizeof(SolveState), cudaMemcpyDeviceToHost, c->stream));
-  RCG_CUDA(c, cudaStreamSynchronize(c->stream));
+  RCG_CUDA_F(cudaMemcpyAsync(hst, st, sizeof(SolveState), cudaMemcpyDeviceToHost, c->stream));
+  RCG_CUDA_F(cudaStreamSynchronize(c->stream));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ev0, ev1);
   cudaEventDestroy(ev0);
@@ -1846,6 +1900,8 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
                                                  : "(w, A w) <= 0: operator not SPD on search space");
   }
   return RCG_OK;
+#undef RCG_CUDA_F
+#undef RCG_LAUNCH_CHECK_F
 }
 
 extern "C" int rcg_apcg_solve(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, const rcg_deflation* D,

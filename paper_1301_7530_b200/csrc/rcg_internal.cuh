@@ -61,6 +61,7 @@ struct Ctx {
   struct Pending {
     int kclass;
     double bytes;
+    int64_t jj;   // solve-loop iteration the launch was queued for (-1: not a loop launch)
     cudaEvent_t a, b;
   };
   std::vector<Pending> pending;
@@ -72,14 +73,24 @@ struct Ctx {
   Comm* comm = nullptr;                  // NCCL communicator (sharded runs)
   void* dargs = nullptr;                 // device-resident solve arguments (graph replay)
   cudaStream_t capture_stream = nullptr; // private stream for graph capture
-  std::map<std::string, std::pair<cudaGraphExec_t, int64_t>> graphs;  // key -> (exec, kernels)
+  struct GraphEntry {
+    cudaGraphExec_t exec;
+    int64_t kernels;   // kernel launches one replay stands for
+    uint64_t last;     // use tick (LRU eviction)
+  };
+  std::map<std::string, GraphEntry> graphs;   // batch shape -> executable graph
+  uint64_t graph_tick = 0;
+  static constexpr size_t kMaxGraphs = 48;    // TRKS (n_c grows every system) keeps adding shapes
 };
 
 // Brackets a launch with events when profiling; `collect` (after a stream
 // sync) folds the elapsed times into the per-class stats.
-void prof_begin(Ctx* c, int kclass, double bytes);
+void prof_begin(Ctx* c, int kclass, double bytes, int64_t jj = -1);
 void prof_end(Ctx* c);
-void prof_collect(Ctx* c);
+// stop_j >= 0: the solve stopped in iteration stop_j; launches queued for later
+// iterations (and the precond / colreduce / w-update launches of stop_j itself,
+// which return at their `done` test) were no-ops and are not counted
+void prof_collect(Ctx* c, int64_t stop_j = -1);
 
 int set_error(Ctx* c, int code, const char* fmt, ...);
 

@@ -458,6 +458,91 @@ int eigvecs(Ctx* c, const double* d, const double* e, int64_t m, const double* v
   return RCG_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// cluster filter (ritz.py:141-183): the best three-segment constant fit of the
+// m-1 gaps between consecutive Ritz values.  Every admissible split (a, b)
+// (cluster = gaps [a, b), at least min_cluster-1 of them) is scored by its
+// own thread; the per-CTA winners are then reduced in one CTA.  Scores use the
+// reference's arithmetic exactly (sequential prefix sums, explicitly rounded
+// products and quotients), so the winning split is the reference's, including
+// its tie order (error, larger cluster, smaller gap level, smaller start).
+
+struct ClusterBest {
+  double err;
+  double level;
+  int64_t size;
+  int64_t a;
+};
+
+__device__ __forceinline__ bool cluster_better(const ClusterBest& x, const ClusterBest& y) {
+  if (x.err != y.err) return x.err < y.err;
+  if (x.size != y.size) return x.size > y.size;
+  if (x.level != y.level) return x.level < y.level;
+  return x.a < y.a;
+}
+
+// one thread: sequential running sums of the gaps and squared gaps
+// (numpy cumsum order), p[0] = 0
+__global__ void cluster_prefix_kernel(const double* __restrict__ v, int64_t m, double* p1, double* p2) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s1 = 0.0, s2 = 0.0;
+  p1[0] = 0.0;
+  p2[0] = 0.0;
+  for (int64_t i = 0; i + 1 < m; ++i) {
+    const double g = fabs(__dsub_rn(v[i + 1], v[i]));
+    s1 = __dadd_rn(s1, g);
+    s2 = __dadd_rn(s2, __dmul_rn(g, g));
+    p1[i + 1] = s1;
+    p2[i + 1] = s2;
+  }
+}
+
+__device__ __forceinline__ double seg_sse(const double* p1, const double* p2, int64_t i, int64_t j) {
+  if (j <= i) return 0.0;
+  const double s = __dsub_rn(p1[j], p1[i]);
+  const double q = __dsub_rn(p2[j], p2[i]);
+  return __dsub_rn(q, __ddiv_rn(__dmul_rn(s, s), (double)(j - i)));
+}
+
+template <int T>
+__device__ void cluster_block_argmin(ClusterBest mine, ClusterBest* out) {
+  __shared__ ClusterBest sb[T];
+  sb[threadIdx.x] = mine;
+  __syncthreads();
+  for (int s = T / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s && cluster_better(sb[threadIdx.x + s], sb[threadIdx.x])) sb[threadIdx.x] = sb[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sb[0];
+}
+
+// CTA q scores the splits whose cluster starts at a = q, q + G, ...; threads
+// sweep the cluster end b
+template <int T>
+__global__ void __launch_bounds__(T) cluster_search_kernel(const double* __restrict__ p1, const double* __restrict__ p2,
+                                                           int64_t ng, int64_t span, ClusterBest* part) {
+  ClusterBest best{INFINITY, INFINITY, -1, INT64_MAX};
+  for (int64_t a = blockIdx.x; a + span <= ng; a += gridDim.x) {
+    const double head = seg_sse(p1, p2, 0, a);
+    for (int64_t b = a + span + threadIdx.x; b <= ng; b += T) {
+      const double err = __dadd_rn(__dadd_rn(head, seg_sse(p1, p2, a, b)), seg_sse(p1, p2, b, ng));
+      const double level = b > a ? __ddiv_rn(__dsub_rn(p1[b], p1[a]), (double)(b - a)) : 0.0;
+      const ClusterBest cand{err, level, b - a, a};
+      if (cluster_better(cand, best)) best = cand;
+    }
+  }
+  cluster_block_argmin<T>(best, part + blockIdx.x);
+}
+
+template <int T>
+__global__ void __launch_bounds__(T) cluster_final_kernel(const ClusterBest* __restrict__ part, int n, ClusterBest* out) {
+  ClusterBest best{INFINITY, INFINITY, -1, INT64_MAX};
+  for (int i = threadIdx.x; i < n; i += T)
+    if (cluster_better(part[i], best)) best = part[i];
+  cluster_block_argmin<T>(best, out);
+}
+
 }  // namespace rcg
 
 using namespace rcg;
@@ -548,4 +633,39 @@ extern "C" int rcg_ritz_vectors(rcg_ctx* ctx, const double* alphas, const double
   }
   cudaFreeAsync(buf, c->stream);
   return rc;
+}
+
+extern "C" int rcg_cluster_filter(rcg_ctx* ctx, const double* values, int64_t m, int64_t min_cluster,
+                                  int64_t* range_host) {
+  if (!ctx || !range_host) return RCG_ERR_CONTRACT;
+  if (min_cluster < 1) return set_error(ctx, RCG_ERR_CONTRACT, "min_cluster must be >= 1");
+  if (m < min_cluster || m < 2) {  // no cluster: every value is kept (ritz.py:158-159)
+    range_host[0] = m;
+    range_host[1] = m - 1;
+    return RCG_OK;
+  }
+  Ctx* c = ctx;
+  const int64_t ng = m - 1, span = min_cluster - 1;
+  const int G = (int)std::min<int64_t>(ng - span + 1, 4 * (int64_t)c->num_sms);
+  constexpr int T = 256;
+  char* buf = nullptr;
+  const size_t bytes = sizeof(double) * 2 * (size_t)m + sizeof(ClusterBest) * (size_t)(G + 1) + 256;
+  RCG_CUDA(c, cudaMallocAsync((void**)&buf, bytes, c->stream));
+  double* p1 = (double*)buf;
+  double* p2 = p1 + m;
+  ClusterBest* part = (ClusterBest*)(((uintptr_t)(p2 + m) + 63) & ~(uintptr_t)63);
+  ClusterBest* fin = part + G;
+  cluster_prefix_kernel<<<1, 32, 0, c->stream>>>(values, m, p1, p2);
+  cluster_search_kernel<T><<<G, T, 0, c->stream>>>(p1, p2, ng, span, part);
+  cluster_final_kernel<T><<<1, T, 0, c->stream>>>(part, G, fin);
+  c->launches += 3;
+  ClusterBest h{};
+  cudaError_t e = cudaMemcpyAsync(&h, fin, sizeof(h), cudaMemcpyDeviceToHost, c->stream);
+  cudaFreeAsync(buf, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return set_error(c, RCG_ERR_CUDA, "cluster filter: %s", cudaGetErrorString(e));
+  // cluster = value indices a .. a + size (ritz.py:182-183)
+  range_host[0] = h.a;
+  range_host[1] = h.a + h.size;
+  return RCG_OK;
 }

@@ -1175,12 +1175,8 @@ int launch_spmv_ind(Ctx* c, const rcg_csr* A, const SpmvArgs* dargs) {
     if (A->dia_block == 3 && dia3_tma() && RCG_DIA_TILED) {
       k = nd == 14 ? dia3t_kernel_ind<14> : dia3t_kernel_ind<0>;
       smem = dia3t_smem();
-      static bool attr14 = false, attr0 = false;
-      bool& done_attr = nd == 14 ? attr14 : attr0;
-      if (!done_attr) {
-        RCG_CUDA(c, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        done_attr = true;
-      }
+      // the attribute is per device: set it on every call (host-side, cheap)
+      RCG_CUDA(c, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
     grid = dia_grid_for(c, A, 1, true);
     if (k) {

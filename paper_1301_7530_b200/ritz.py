@@ -172,37 +172,22 @@ def select_converged(current: RitzSpectrum, previous_values, epsilon) -> RitzSpe
 
 
 def cluster_filter(values, min_cluster):
-    """Indices of values outside the central dense cluster (``ritz.py:141-183``).
+    """Indices of values outside the central dense cluster (drop-in for
+    ``ritz.py:141-183``).
 
-    Host-side by design: O(m^2) scalar work on the m Ritz values of one solve,
-    outside the iteration (SURVEY.md §2 marks it out of the device scope).
+    The split search runs on the device (``rcg_cluster_filter``): one thread
+    per candidate cluster [a, b], scored with the reference's own arithmetic
+    and tie order, then a fixed-order argmin.  ``values`` may be a host array
+    or a CUDA tensor (descending Ritz values).
     """
-    values = np.asarray(values, dtype=np.float64)
     m = len(values)
     if min_cluster < 1:
         raise ContractViolation("min_cluster must be >= 1")
     if m < min_cluster or m < 2:
         return list(range(m))
-    gaps = np.abs(np.diff(values))
-    ng = len(gaps)
-    s1 = np.concatenate([[0.0], np.cumsum(gaps)])
-    s2 = np.concatenate([[0.0], np.cumsum(gaps ** 2)])
-
-    def sse(i, j):
-        if j <= i:
-            return 0.0
-        s = s1[j] - s1[i]
-        return (s2[j] - s2[i]) - s * s / (j - i)
-
-    def level(i, j):
-        return (s1[j] - s1[i]) / (j - i) if j > i else 0.0
-
-    best = None
-    span = min_cluster - 1
-    for lo in range(0, ng - span + 1):
-        for hi in range(lo + span, ng + 1):
-            key = (sse(0, lo) + sse(lo, hi) + sse(hi, ng), -(hi - lo), level(lo, hi), lo)
-            if best is None or key < best[0]:
-                best = (key, lo, hi)
-    _, lo, hi = best
-    return [i for i in range(m) if i < lo or i > hi]
+    vd, _ = to_dev(values)
+    rng = (_lib.C.c_int64 * 2)()
+    ctx = _lib.context()
+    ctx.check(ctx.lib.rcg_cluster_filter(ctx.h, _lib.ptr(vd), m, int(min_cluster), rng), "cluster_filter")
+    lo, hi = int(rng[0]), int(rng[1])
+    return list(range(lo)) + list(range(hi + 1, m))

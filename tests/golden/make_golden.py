@@ -11,6 +11,7 @@ from __future__ import annotations
 import hashlib
 import json
 import sys
+import time
 from pathlib import Path
 
 import numpy as np
@@ -188,6 +189,147 @@ def pilot_fixture():
     (HERE / "benchmark_pilot_none_trks.json").write_text(json.dumps(keep, indent=1) + "\n")
 
 
+# ---------------------------------------------------------------------------
+# round 2: sequence-level goldens at the BASELINE configs
+
+
+def _sample_idx(n, count=16384, seed=7):
+    """Seeded index sample used to pin large solutions without storing them."""
+    rng = np.random.Generator(np.random.Philox(seed))
+    return np.sort(rng.choice(n, size=min(n, count), replace=False))
+
+
+def _spy_sequence(systems, strat, cfg, C0=None, keep_x=(), sample=None):
+    """Run the REFERENCE run_sequence unchanged, spying on its apcg_solve and
+    select_spectrum seams (recycle.py:204, :218) to record each system's
+    solution (or a seeded sample of it) and its selected Ritz values."""
+    xs, sel = {}, []
+    real_solve, real_select = ref_recycle.apcg_solve, ref_recycle.select_spectrum
+    k_box = [0]
+
+    def solve(A, M, D, b, c):
+        x, tr = real_solve(A, M, D, b, c)
+        k = k_box[0]
+        k_box[0] += 1
+        if k in keep_x:
+            xs[k] = x.copy() if sample is None else x[sample].copy()
+        return x, tr
+
+    def select(trace, strategy):
+        spec = real_select(trace, strategy)
+        sel.append((k_box[0] - 1, [float(v) for v in spec.values[spec.converged_mask]]))
+        return spec
+
+    ref_recycle.apcg_solve, ref_recycle.select_spectrum = solve, select
+    try:
+        rep = ref_recycle.run_sequence(iter(systems), recycg.Preconditioner.jacobi, strat, cfg, C0)
+    finally:
+        ref_recycle.apcg_solve, ref_recycle.select_spectrum = real_solve, real_select
+    per_step = [[] for _ in rep.records]
+    for k, vals in sel:
+        if k < len(per_step):
+            per_step[k] = vals
+    return rep, xs, per_step
+
+
+def _report_dict(rep):
+    return dict(iterations=rep.iterations(), n_c_before=rep.n_c_history(),
+                n_c_selected=[r.n_c_selected for r in rep.records],
+                final_residual=[r.final_residual for r in rep.records],
+                converged=[bool(r.converged) for r in rep.records], aborted=bool(rep.aborted),
+                events=[list(map(str, e)) for e in rep.events])
+
+
+def reduced_sequences(which=("c2r", "c3r", "c4r_on", "c4r_off", "c5r")):
+    """SURVEY.md §8(d) reduced analogs of configs 2-5 through the reference
+    run_sequence: elasticity 16^3 (20 RHS), 24^3 softening (15 systems),
+    diffusion 64^3 (20 systems, reorth on and off), lognormal-softening
+    elasticity 16^3 (10 systems, nc_limit 101, reorth off)."""
+    out_path = HERE / "reduced_sequences.json"
+    out = json.loads(out_path.read_text()) if out_path.exists() else {}
+    sols = dict(np.load(HERE / "reduced_solutions.npz")) if (HERE / "reduced_solutions.npz").exists() else {}
+    specs = {
+        "c2r": (2, True), "c3r": (3, True), "c4r_on": (4, True), "c4r_off": (4, False), "c5r": (5, False),
+    }
+    for name in which:
+        config, reorth = specs[name]
+        systems, st = problems.config_systems(config, reduced=True)
+        systems = list(systems)
+        shas = [csr_sha(A) for A, _ in systems]
+        bsha = [hashlib.sha256(b.tobytes()).hexdigest() for _, b in systems]
+        ref_systems = [(to_ref(A), b) for A, b in systems]
+        cfg = recycg.SolveConfig(tol=st["tol"], max_iters=5000, reorthogonalize=reorth)
+        strat = recycg.RecycleStrategy("srks", epsilon=st["epsilon"], nc_limit=st["nc_limit"])
+        last = len(systems) - 1
+        t0 = time.time()
+        n0 = systems[0][0].n
+        sample = _sample_idx(n0) if n0 > 50000 else None      # large n: pin a seeded sample of x
+        rep, xs, per_step = _spy_sequence(ref_systems, strat, cfg, keep_x=(0, 1, last), sample=sample)
+        d = _report_dict(rep)
+        d.update(config=config, reduced=True, reorthogonalize=reorth, tol=st["tol"], epsilon=st["epsilon"],
+                 nc_limit=st["nc_limit"], n=int(systems[0][0].n), nnz=int(systems[0][0].nnz),
+                 matrix_sha256=shas, rhs_sha256=bsha, selected_ritz_values=per_step,
+                 reference_seconds=time.time() - t0)
+        out[name] = d
+        for k, x in xs.items():
+            sols[f"{name}__x{k}"] = x
+        out_path.write_text(json.dumps(out, indent=1) + "\n")
+        np.savez_compressed(HERE / "reduced_solutions.npz", **sols)
+        print(name, d["iterations"], d["n_c_before"], f"{d['reference_seconds']:.0f}s", flush=True)
+
+
+def config2_full(count=2):
+    """BASELINE config 2 at full size (Q1 64^3, n = 811,200), systems 0..count-1
+    through the reference run_sequence: SRKS eps 1e-10, nc_limit 61, tol 1e-8,
+    full reorth.  Solutions are pinned on a seeded 16,384-entry sample plus
+    their norms."""
+    gen = problems.elasticity_sequence(64, count, kind="fixed")
+    systems = list(gen)
+    A = systems[0][0]
+    idx = _sample_idx(A.n)
+    Ar = to_ref(A)
+    cfg = recycg.SolveConfig(tol=1e-8, max_iters=20000)
+    strat = recycg.RecycleStrategy("srks", epsilon=1e-10, nc_limit=61)
+    t0 = time.time()
+    rep, xs, per_step = _spy_sequence([(Ar, b) for _, b in systems], strat, cfg, keep_x=tuple(range(count)))
+    d = _report_dict(rep)
+    d.update(n=int(A.n), nnz=int(A.nnz), matrix_sha256=csr_sha(A),
+             rhs_sha256=[hashlib.sha256(b.tobytes()).hexdigest() for _, b in systems],
+             selected_ritz_values=per_step, reference_seconds=time.time() - t0,
+             x_norm=[float(np.linalg.norm(xs[k])) for k in range(count)], sample_seed=7)
+    (HERE / "config2_full.json").write_text(json.dumps(d, indent=1) + "\n")
+    np.savez_compressed(HERE / "config2_full_xsample.npz", idx=idx,
+                        **{f"x{k}": xs[k][idx] for k in range(count)})
+    print("config2 full", d["iterations"], d["n_c_before"], f"{d['reference_seconds']:.0f}s", flush=True)
+
+
+def acceptance6():
+    """Reference acceptance criterion 6 (pkg/tests/test_acceptance.py:226-266)
+    restated: the 40-system inclusion benchmark with none / trks / srks(1e-14)
+    at tol 1e-3 and trks / srks(1e-14) at tol 1e-6, run through the reference
+    here; the frozen margins come from the reference fixture."""
+    fx = json.loads(Path("/root/reference/pkg/tests/fixtures/benchmark_pilot.json").read_text())
+    ref_systems = list(ref_problems.generate_diffusion_sequence(ref_problems.benchmark_spec(seed=0), 40))
+    mine = list(problems.generate_diffusion_sequence(problems.benchmark_spec(seed=0), 40))
+    for (Ar, br), (Am, bm) in zip(ref_systems, mine):
+        assert csr_sha(Ar) == csr_sha(Am) and np.array_equal(br, bm), "benchmark generator drifted"
+    out = {"margins": fx["margins"], "matrix_sha256": [csr_sha(A) for A, _ in mine]}
+    for tol, runs in [(1e-3, [("none", "none", None), ("trks", "trks", None), ("srks14", "srks", 1e-14)]),
+                      (1e-6, [("trks", "trks", None), ("srks14", "srks", 1e-14)])]:
+        cfg = recycg.SolveConfig(tol=tol, max_iters=3000)
+        for name, kind, eps in runs:
+            strat = recycg.RecycleStrategy(kind, **({"epsilon": eps} if eps else {}))
+            t0 = time.time()
+            rep = recycg.run_sequence(iter(ref_systems), recycg.Preconditioner.jacobi, strat, cfg)
+            d = _report_dict(rep)
+            d["reference_seconds"] = time.time() - t0
+            out.setdefault(f"tol{tol:g}", {})[name] = d
+            print("accept6", tol, name, d["iterations"][:6], d["n_c_before"][-3:], f"{d['reference_seconds']:.0f}s",
+                  flush=True)
+    (HERE / "acceptance6.json").write_text(json.dumps(out, indent=1) + "\n")
+
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["small", "config1", "bench", "elast", "pilot"]
     if "pilot" in which:
@@ -200,3 +342,11 @@ if __name__ == "__main__":
         benchmark_srks()
     if "config1" in which:
         config1_sequence()
+    for w in which:
+        if w.startswith("reduced"):
+            names = w.split(":")[1].split(",") if ":" in w else None
+            reduced_sequences(*( [names] if names else []))
+    if "config2" in which:
+        config2_full()
+    if "accept6" in which:
+        acceptance6()
