@@ -1174,7 +1174,15 @@ static int rows_per_block_for(const Ctx* c, int64_t n) {
 
 static int rows_per_block_for(const Ctx* c, int64_t n, int tiles_per_sm) {
   // ~4 row tiles per SM: the tile kernels run 3-4 CTAs/SM (45 KB smem, <= 64 regs)
-  int64_t rpt = ceil_div(n, (int64_t)kThreads * tiles_per_sm * c->num_sms);
+  const int64_t wave_rows = (int64_t)kThreads * tiles_per_sm * c->num_sms;   // one wave at 1 row/thread
+  int64_t rpt = ceil_div(n, wave_rows);
+  if (rpt > 16) {
+    // the tile is capped (smem: 2 x 16 x 256 doubles); size it so the tiles
+    // fill whole waves of resident CTAs instead of leaving a short last wave
+    // (config 3, n = 2.7 M: 662 tiles = 2.24 waves -> 883 tiles = 2.98 waves)
+    const int64_t waves = ceil_div(rpt, (int64_t)16);
+    rpt = ceil_div(n, wave_rows * waves);
+  }
   rpt = std::max<int64_t>(1, std::min<int64_t>(rpt, 16));
   return (int)(rpt * kThreads);
 }
