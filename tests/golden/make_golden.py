@@ -330,6 +330,22 @@ def acceptance6():
 
 
 
+def trks_config1(count=5):
+    """TRKS on config 1 at tol 1e-8 (the explicit G^-1 coarse
+    solve against a high-kappa C^T A C): normalized directions make kappa(G)
+    ~ kappa(A).  Reference run_sequence, first `count` systems."""
+    systems = problems.shifted_laplacian_sequence(count=count)
+    ref_systems = [(to_ref(A), b) for A, b in systems]
+    cfg = recycg.SolveConfig(tol=1e-8, max_iters=2000)
+    t0 = time.time()
+    rep, xs, _ = _spy_sequence(ref_systems, recycg.RecycleStrategy("trks"), cfg, keep_x=tuple(range(count)))
+    d = _report_dict(rep)
+    d["reference_seconds"] = time.time() - t0
+    (HERE / "trks_config1.json").write_text(json.dumps(d, indent=1) + "\n")
+    np.savez_compressed(HERE / "trks_config1_solutions.npz", **{f"x{k}": x for k, x in xs.items()})
+    print("trks config1", d["iterations"], d["n_c_before"], f"{d['reference_seconds']:.0f}s", flush=True)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["small", "config1", "bench", "elast", "pilot"]
     if "pilot" in which:
@@ -350,3 +366,5 @@ if __name__ == "__main__":
         config2_full()
     if "accept6" in which:
         acceptance6()
+    if "trks1" in which:
+        trks_config1()

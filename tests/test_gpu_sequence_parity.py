@@ -302,3 +302,32 @@ def test_acceptance_criterion_6_sequence_benchmark():
         assert all(abs(a - b) <= max(2, 0.02 * b) for a, b in zip(got.n_c_history(), want["n_c_before"])), \
             (got.n_c_history(), want["n_c_before"])
     assert max(ncs_t) > 1500                  # the large-n_c coarse path really ran
+
+
+# ---------------------------------------------------------------------------
+# TRKS with a high-kappa coarse matrix: config 1 at tol 1e-8,
+# n_c grows 0 -> 723; the coarse solve applies the explicit G^-1 = L^-T L^-1
+
+
+def test_trks_config1_high_kappa_coarse_matches_reference(monkeypatch):
+    path = GOLDEN / "trks_config1.json"
+    if not path.exists():
+        pytest.skip("trks golden not generated")
+    g = json.loads(path.read_text())
+    sols = np.load(GOLDEN / "trks_config1_solutions.npz")
+    count = len(g["iterations"])
+    systems = problems.shifted_laplacian_sequence(count=count)
+    spy = Spy(monkeypatch, keep_x=tuple(range(count)))
+    for path_kind in ("persistent", "multi_kernel"):
+        if path_kind == "multi_kernel":
+            monkeypatch.setenv("RCG_SMALL_N", "0")
+        spy.k = -1
+        rep = rcg.run_sequence(iter(systems), rcg.Preconditioner.jacobi, rcg.RecycleStrategy("trks"),
+                               rcg.SolveConfig(tol=1e-8, max_iters=2000))
+        got, want = rep.iterations(), g["iterations"]
+        assert all(_close(a, b) for a, b in zip(got, want)), (path_kind, got, want)
+        assert all(abs(a - b) <= max(2, 0.02 * b) for a, b in zip(rep.n_c_history(), g["n_c_before"])), \
+            (path_kind, rep.n_c_history(), g["n_c_before"])
+        for k in range(count):
+            want_x = sols[f"x{k}"]
+            assert np.linalg.norm(spy.x[k] - want_x) <= 1e-8 * np.linalg.norm(want_x), (path_kind, k)
