@@ -151,7 +151,46 @@ __device__ __forceinline__ void gemv_t_tile(const double* __restrict__ base, int
       const int kc = (int)min((int64_t)CG, ncols - k0);
       const double* __restrict__ cols = base + k0 * ld;
       const int64_t p_begin = sl * per, p_end = min(pairs, p_begin + per);
-      if (kc == CG) {
+      if (kc == CG && !PF) {
+        // explicit batch: the CG 128-bit loads of two consecutive steps are
+        // issued before any FMA (the compiler, at the 128-register budget,
+        // otherwise interleaves them with the FMAs and keeps only ~4 loads in
+        // flight: tools/k3_layout_bench.cu, 6.96 -> 7.12 TB/s at config 3).
+        // Accumulation order per column is unchanged (step p, then p + 32).
+        int64_t pi = p_begin + lane;
+        for (; pi + 32 < p_end; pi += 64) {
+          double2 va[CG], vb[CG];
+#pragma unroll
+          for (int c = 0; c < CG; ++c) va[c] = __ldcs(reinterpret_cast<const double2*>(cols + c * ld) + pi);
+#pragma unroll
+          for (int c = 0; c < CG; ++c) vb[c] = __ldcs(reinterpret_cast<const double2*>(cols + c * ld) + pi + 32);
+          const double2 x0a = *reinterpret_cast<const double2*>(v0 + 2 * pi);
+          const double2 x0b = *reinterpret_cast<const double2*>(v0 + 2 * (pi + 32));
+          double2 x1a = make_double2(0.0, 0.0), x1b = make_double2(0.0, 0.0);
+          if (NV == 2) {
+            x1a = *reinterpret_cast<const double2*>(v1 + 2 * pi);
+            x1b = *reinterpret_cast<const double2*>(v1 + 2 * (pi + 32));
+          }
+#pragma unroll
+          for (int c = 0; c < CG; ++c) {
+            a0[c] = fma(va[c].y, x0a.y, fma(va[c].x, x0a.x, a0[c]));
+            if (NV == 2) a1[c] = fma(va[c].y, x1a.y, fma(va[c].x, x1a.x, a1[c]));
+            a0[c] = fma(vb[c].y, x0b.y, fma(vb[c].x, x0b.x, a0[c]));
+            if (NV == 2) a1[c] = fma(vb[c].y, x1b.y, fma(vb[c].x, x1b.x, a1[c]));
+          }
+        }
+        if (pi < p_end) {
+          const double2 x0 = *reinterpret_cast<const double2*>(v0 + 2 * pi);
+          double2 x1 = make_double2(0.0, 0.0);
+          if (NV == 2) x1 = *reinterpret_cast<const double2*>(v1 + 2 * pi);
+#pragma unroll
+          for (int c = 0; c < CG; ++c) {
+            const double2 v = __ldcs(reinterpret_cast<const double2*>(cols + c * ld) + pi);
+            a0[c] += v.x * x0.x + v.y * x0.y;
+            if (NV == 2) a1[c] += v.x * x1.x + v.y * x1.y;
+          }
+        }
+      } else if (kc == CG) {
         if (PF && lane < CG && p_begin < p_end)
           bulk_prefetch_l2(cols + lane * ld + 2 * p_begin,
                            (unsigned)(16 * min((int64_t)32 * PF_DIST, p_end - p_begin)));
@@ -1389,7 +1428,20 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     return (int)std::max<int64_t>(R0, rmin);
   };
   // without reorth K3 is the lean 4-CTA/SM variant: at most one wave of tiles
-  const int R = reorth ? rows_per_block_for(c, n) : big_tile(rows_per_block_for(c, n), 4);
+  // with reorth, K3 tiles (2 x R doubles of smem each) come in whole waves of
+  // resident CTAs (RCG_PRE_MINB per SM): tiles = resident x waves, R a
+  // multiple of 64 rows <= 4096; RCG_PRE_WAVES raises the wave count
+  // (smaller tiles: CTAs drift apart, so one CTA's z pass and reduction tail
+  // overlap other CTAs' AW streams)
+  auto pre_tile = [&]() -> int {
+    static const int min_waves = env_int("RCG_PRE_WAVES", 1);
+    const int64_t resident = (int64_t)RCG_PRE_MINB * c->num_sms;
+    if (n <= resident * 1024) return rows_per_block_for(c, n);
+    const int64_t waves = std::max<int64_t>(min_waves, ceil_div(n, resident * 4096));
+    const int64_t Rr = ceil_div(ceil_div(n, resident * waves), (int64_t)64) * 64;
+    return (int)std::max<int64_t>(64, std::min<int64_t>(Rr, 4096));
+  };
+  const int R = reorth ? pre_tile() : big_tile(rows_per_block_for(c, n), 4);
   const int nb = (int)std::max<int64_t>(1, ceil_div(n, R));
   static const int upd_tiles = env_int("RCG_UPD_TILES_PER_SM", 4);
   const int Ru = n_c ? rows_per_block_for(c, n, upd_tiles) : big_tile(rows_per_block_for(c, n, upd_tiles), 8);

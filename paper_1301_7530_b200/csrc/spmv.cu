@@ -30,6 +30,11 @@
 
 namespace rcg {
 
+template <typename RO>
+__device__ __forceinline__ int64_t nnz_of(const RO* __restrict__ ro, int64_t n) {
+  return (int64_t)__ldg(ro + n);
+}
+
 template <typename RO, int V, int MODE>
 __device__ __forceinline__ void spmv_body(int64_t n, const RO* __restrict__ ro, const int32_t* __restrict__ ci,
                                           const double* __restrict__ va, const ColSel& xs, const ColSel& ys,
@@ -50,6 +55,7 @@ __device__ __forceinline__ void spmv_body(int64_t n, const RO* __restrict__ ro, 
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   double acc0 = 0.0, acc1 = 0.0;
+  const int64_t nnz_all = V >= 2 ? nnz_of(ro, n) : 0;
   int64_t r0 = warp * RPW;
   int64_t rs = 0, re = 0;
   if (r0 < n) {
@@ -72,7 +78,39 @@ __device__ __forceinline__ void spmv_body(int64_t n, const RO* __restrict__ ro, 
     }
     double s = 0.0;
     const bool fast = __all_sync(0xffffffffu, (re - rs) <= (int64_t)U * V);
-    if (fast) {
+    if (V >= 2 && fast) {
+      // 128-bit value / 64-bit index loads: the row's entries as aligned pairs
+      // (2p, 2p+1), lane `sub` takes pairs ps + sub, ps + sub + V, ...; the
+      // entries of a boundary pair outside [rs, re) are masked (no gather).
+      // A pair that would read past nnz falls back to one scalar load.
+      constexpr int UP = U / 2 + 1;            // <= U V entries span <= U V / 2 + 1 pairs
+      const int64_t ps = rs >> 1, pe = (re + 1) >> 1;
+      int2 c[UP];
+      double2 v[UP];
+#pragma unroll
+      for (int u = 0; u < UP; ++u) {
+        const int64_t p = ps + sub + (int64_t)u * V;
+        c[u] = make_int2(0, 0);
+        v[u] = make_double2(0.0, 0.0);
+        if (p < pe) {
+          if (2 * p + 1 < nnz_all) {
+            c[u] = __ldg(reinterpret_cast<const int2*>(ci) + p);
+            v[u] = __ldcs(reinterpret_cast<const double2*>(va) + p);
+          } else {
+            c[u].x = __ldg(ci + 2 * p);
+            v[u].x = __ldcs(va + 2 * p);
+          }
+        }
+      }
+      double t[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int u = 0; u < UP; ++u) {
+        const int64_t k0 = 2 * (ps + sub + (int64_t)u * V);
+        if (k0 >= rs && k0 < re) t[u & 3] += v[u].x * __ldg(x + c[u].x);
+        if (k0 + 1 >= rs && k0 + 1 < re) t[(u + 2) & 3] += v[u].y * __ldg(x + c[u].y);
+      }
+      s = (t[0] + t[1]) + (t[2] + t[3]);
+    } else if (fast) {
       // every index/value load of the row in flight at once, then every gather
       int c[U];
       double v[U];
