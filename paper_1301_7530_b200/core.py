@@ -56,6 +56,71 @@ def from_dev(t, host):
     return t.cpu().numpy() if host else t
 
 
+class _Stager:
+    """Host -> device upload of large arrays through a ring of pinned staging
+    buffers: host threads copy chunk i + 1 into pinned memory (numpy releases
+    the GIL) while the copy engine moves chunk i, so a 2.6 GB CSR (config 3)
+    crosses at PCIe speed instead of through the driver's single-threaded
+    pageable bounce buffer (0.24 s -> ~0.06 s per operator)."""
+
+    CHUNK = 64 << 20
+    NBUF = 4
+    THREADS = 8
+
+    def __init__(self):
+        torch = _torch()
+        from concurrent.futures import ThreadPoolExecutor
+        self.bufs = [torch.empty(self.CHUNK, dtype=torch.uint8, pin_memory=True) for _ in range(self.NBUF)]
+        self.views = [b.numpy() for b in self.bufs]
+        self.events = [None] * self.NBUF
+        self.stream = torch.cuda.Stream()
+        self.pool = ThreadPoolExecutor(self.THREADS)
+
+    def _fill(self, dst, src):
+        n = len(src)
+        step = -(-n // self.THREADS)
+        parts = [(dst[i:i + step], src[i:i + step]) for i in range(0, n, step)]
+        list(self.pool.map(lambda p: np.copyto(p[0], p[1]), parts))
+
+    def upload(self, arr):
+        torch = _torch()
+        arr = np.ascontiguousarray(arr)
+        out = torch.empty(arr.shape, dtype=getattr(torch, str(arr.dtype)), device="cuda")
+        src = arr.reshape(-1).view(np.uint8)
+        dst = out.view(-1).view(torch.uint8)
+        self.stream.wait_stream(torch.cuda.current_stream())   # `out` was allocated on the current stream
+        for i, off in enumerate(range(0, len(src), self.CHUNK)):
+            k = i % self.NBUF
+            if self.events[k] is not None:
+                self.events[k].synchronize()                     # its previous DMA has drained
+            nb = min(self.CHUNK, len(src) - off)
+            self._fill(self.views[k][:nb], src[off:off + nb])
+            with torch.cuda.stream(self.stream):
+                dst[off:off + nb].copy_(self.bufs[k][:nb], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.stream)
+            self.events[k] = ev
+        torch.cuda.current_stream().wait_stream(self.stream)
+        out.record_stream(self.stream)
+        return out
+
+
+_stagers = {}
+
+
+def h2d(arr):
+    """Device copy of a host array; large arrays go through the pinned ring."""
+    torch = _torch()
+    arr = np.asarray(arr)
+    if arr.nbytes < (32 << 20) or _os.environ.get("RCG_PINNED_UPLOAD", "1") == "0":
+        return torch.from_numpy(np.ascontiguousarray(arr)).to("cuda")
+    dev = torch.cuda.current_device()
+    st = _stagers.get(dev)
+    if st is None:
+        st = _stagers[dev] = _Stager()
+    return st.upload(arr)
+
+
 def pad_ld(n):
     return max(32, ((int(n) + 31) // 32) * 32)
 
@@ -253,9 +318,9 @@ class SparseSpdMatrix:
         h = self._dev.get(dev)
         if h is None:
             ro64 = self.nnz >= 2 ** 31 - 1
-            ro = torch.from_numpy(self.row_offsets.astype(np.int64 if ro64 else np.int32)).to("cuda")
-            ci = torch.from_numpy(np.ascontiguousarray(self.col_indices, dtype=np.int32)).to("cuda")
-            va = torch.from_numpy(self.values).to("cuda")
+            ro = h2d(self.row_offsets.astype(np.int64 if ro64 else np.int32))
+            ci = h2d(np.ascontiguousarray(self.col_indices, dtype=np.int32))
+            va = h2d(self.values)
             h = _DevCsr(ro, ci, va, self.n, self.nnz, ro64)
             _maybe_block3(h, self.n, self.nnz, self.use_block3)
             self._dev[dev] = h

@@ -249,6 +249,173 @@ chol_col_kernel(int64_t n, int64_t j, const double* __restrict__ G, double* L, d
   }
 }
 
+// Blocked guarded Cholesky for n > 128 (TRKS bases reach n_c ~ 1.6 k):
+// panels of CHOL_NB columns, three launches per panel -
+//   (1) chol_update_kernel: A[p0:, p0:p0+nb] -= L[p0:, :p0] L[p0:p0+nb, :p0]^T
+//       (left-looking GEMM, 64 x 64 tiles, fixed k order);
+//   (2) chol_diag_kernel: one CTA factors the nb x nb diagonal block in smem
+//       with the pivot rule (running max of the pivots in pivmax[0]);
+//   (3) chol_trsm_kernel: L21 = A21 L11^-T, one thread per row, L11 in smem.
+// L holds the working matrix (lower triangle of G copied in first).  A failed
+// pivot sets *bad and every later launch returns at entry.
+constexpr int CHOL_NB = 64;
+
+__global__ void __launch_bounds__(256)
+chol_update_kernel(int64_t n, int64_t p0, int nb, double* L, const long long* bad) {
+  if (*bad >= 0) return;
+  __shared__ double As[32][64 + 1];   // [k][row]
+  __shared__ double Bs[32][64 + 1];   // [k][panel column]
+  const int t = threadIdx.x, tr = t & 15, tc = t >> 4;
+  const int64_t i0 = p0 + (int64_t)blockIdx.x * 64;
+  double acc[4][4] = {};
+  for (int64_t k0 = 0; k0 < p0; k0 += 32) {
+    for (int idx = t; idx < 32 * 64; idx += 256) {
+      const int kk = idx >> 6, rr = idx & 63;
+      const int64_t k = k0 + kk, i = i0 + rr, c = p0 + rr;
+      As[kk][rr] = (k < p0 && i < n) ? L[k * n + i] : 0.0;
+      Bs[kk][rr] = (k < p0 && rr < nb) ? L[k * n + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < 32; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = As[kk][tr + 16 * u];
+        b[u] = Bs[kk][tc + 16 * u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int64_t i = i0 + tr + 16 * u;
+      const int c = tc + 16 * v;
+      if (i < n && c < nb && i >= p0 + c) L[(p0 + c) * n + i] -= acc[u][v];
+    }
+}
+
+__global__ void __launch_bounds__(1024)
+chol_diag_kernel(int64_t n, int64_t p0, int nb, double* L, double* pivmax, double pivot_rtol, long long* bad) {
+  if (*bad >= 0) return;
+  __shared__ double A[CHOL_NB * CHOL_NB];   // nb x nb, column-major
+  __shared__ double s_piv;
+  __shared__ int s_bad;
+  const int t = threadIdx.x, nt = blockDim.x;
+  for (int idx = t; idx < nb * nb; idx += nt) {
+    const int i = idx % nb, c = idx / nb;
+    A[idx] = i >= c ? L[(p0 + c) * n + p0 + i] : 0.0;
+  }
+  if (t == 0) {
+    s_piv = *pivmax;
+    s_bad = -1;
+  }
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    const double d = A[j * nb + j];
+    const double top = s_piv;
+    if (d <= top * pivot_rtol || d <= 0.0 || !isfinite(d)) {
+      if (t == 0) s_bad = j;
+      break;  // uniform
+    }
+    const double ljj = sqrt(d);
+    __syncthreads();
+    if (t == 0) s_piv = fmax(top, d);
+    for (int i = j + 1 + t; i < nb; i += nt) A[j * nb + i] /= ljj;
+    __syncthreads();
+    if (t == 0) A[j * nb + j] = ljj;
+    const int m = nb - j - 1;
+    for (int idx = t; idx < m * m; idx += nt) {
+      const int kk = j + 1 + idx / m, i = j + 1 + idx % m;
+      if (i >= kk) A[kk * nb + i] -= A[j * nb + i] * A[j * nb + kk];
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  for (int idx = t; idx < nb * nb; idx += nt) {
+    const int i = idx % nb, c = idx / nb;
+    if (i >= c) L[(p0 + c) * n + p0 + i] = A[idx];
+  }
+  if (t == 0) {
+    *pivmax = s_piv;
+    if (s_bad >= 0) *bad = p0 + s_bad;
+  }
+}
+
+constexpr int CHOL_TRSM_ROWS = 128;
+
+__global__ void __launch_bounds__(CHOL_TRSM_ROWS)
+chol_trsm_kernel(int64_t n, int64_t p0, int nb, double* L, const long long* bad) {
+  if (*bad >= 0) return;
+  extern __shared__ double trsm_sm[];
+  double* L11 = trsm_sm;                                // nb x nb, column-major
+  double* X = trsm_sm + CHOL_NB * CHOL_NB;              // [c][thread]
+  const int t = threadIdx.x;
+  for (int idx = t; idx < nb * nb; idx += CHOL_TRSM_ROWS) {
+    const int i = idx % nb, c = idx / nb;
+    L11[idx] = i >= c ? L[(p0 + c) * n + p0 + i] : 0.0;
+  }
+  const int64_t i = p0 + nb + (int64_t)blockIdx.x * CHOL_TRSM_ROWS + t;
+  for (int c = 0; c < nb; ++c) X[c * CHOL_TRSM_ROWS + t] = i < n ? L[(p0 + c) * n + i] : 0.0;
+  __syncthreads();
+  if (i >= n) return;
+  for (int c = 0; c < nb; ++c) {           // x_c = (a_c - sum_{k<c} x_k L11[c, k]) / L11[c, c]
+    double s = X[c * CHOL_TRSM_ROWS + t];
+    for (int k = 0; k < c; ++k) s -= X[k * CHOL_TRSM_ROWS + t] * L11[k * nb + c];
+    X[c * CHOL_TRSM_ROWS + t] = s / L11[c * nb + c];
+  }
+  for (int c = 0; c < nb; ++c) L[(p0 + c) * n + i] = X[c * CHOL_TRSM_ROWS + t];
+}
+
+__global__ void copy_lower_kernel(int64_t n, const double* __restrict__ G, double* L) {
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n * n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx % n, c = idx / n;
+    L[idx] = i >= c ? G[idx] : 0.0;
+  }
+}
+
+// Lt = L^T (so row i of L is contiguous for the warp-per-column inverse)
+__global__ void transpose_kernel(int64_t n, const double* __restrict__ L, double* Lt) {
+  __shared__ double tile[32][33];
+  const int64_t bx = (int64_t)blockIdx.x * 32, by = (int64_t)blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t i = bx + threadIdx.x, c = by + r;
+    tile[r][threadIdx.x] = (i < n && c < n) ? L[c * n + i] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t c = by + threadIdx.x, i = bx + r;
+    if (i < n && c < n) Lt[i * n + c] = tile[threadIdx.x][r];
+  }
+}
+
+// Linv = L^{-1}, one warp per column c: Linv[i, c] = (delta_ic - sum_{c<=k<i}
+// L[i, k] Linv[k, c]) / L[i, i], the sum split over the lanes (contiguous
+// rows of Lt) and warp-reduced in a fixed order
+__global__ void __launch_bounds__(256)
+trtri_warp_kernel(int64_t n, const double* __restrict__ Lt, double* Linv) {
+  const int lane = threadIdx.x & 31;
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (c >= n) return;
+  double* col = Linv + c * n;
+  for (int64_t i = lane; i < c; i += 32) col[i] = 0.0;
+  for (int64_t i = c; i < n; ++i) {
+    const double* row = Lt + i * n;
+    double p = 0.0;
+    for (int64_t k = c + lane; k < i; k += 32) p += row[k] * col[k];
+    p = warp_sum(p);
+    if (lane == 0) col[i] = ((i == c ? 1.0 : 0.0) - p) / row[i];
+    __syncwarp();
+  }
+}
+
 // Linv = L^{-1} (lower), one thread per column, forward substitution
 __global__ void trtri_lower_kernel(int64_t n, const double* __restrict__ L, double* Linv) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -278,7 +445,7 @@ int cholesky(Ctx* c, const double* G, int64_t n, double pivot_rtol, double* L, d
                                      (int)std::max<size_t>(smem, 48 * 1024)));
     chol_smem_kernel<<<1, 1024, smem, c->stream>>>((int)n, G, pivot_rtol, L, bad);
     RCG_LAUNCH_CHECK(c);
-  } else {
+  } else if (getenv("RCG_CHOL_COLUMNS")) {   // the per-column left-looking kernel (A/B reference)
     RCG_CUDA(c, cudaMemsetAsync(L, 0, sizeof(double) * (size_t)n * n, c->stream));
     RCG_CUDA(c, cudaMemsetAsync(pivmax, 0, sizeof(double) * (size_t)(n + 1), c->stream));
     RCG_CUDA(c, cudaMemsetAsync(bad, 0xff, sizeof(long long), c->stream));  // -1
@@ -286,6 +453,28 @@ int cholesky(Ctx* c, const double* G, int64_t n, double pivot_rtol, double* L, d
       const int g = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n - j, 256), c->num_sms));
       chol_col_kernel<<<g, 256, 0, c->stream>>>(n, j, G, L, pivmax, pivot_rtol, bad);
       RCG_LAUNCH_CHECK(c);
+    }
+  } else {
+    RCG_CUDA(c, cudaMemsetAsync(pivmax, 0, sizeof(double), c->stream));
+    RCG_CUDA(c, cudaMemsetAsync(bad, 0xff, sizeof(long long), c->stream));  // -1
+    copy_lower_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n * n, 256), 8 * c->num_sms), 256, 0, c->stream>>>(
+        n, G, L);
+    RCG_LAUNCH_CHECK(c);
+    for (int64_t p0 = 0; p0 < n; p0 += CHOL_NB) {
+      const int nb = (int)std::min<int64_t>(CHOL_NB, n - p0);
+      if (p0 > 0) {
+        chol_update_kernel<<<(unsigned)ceil_div(n - p0, (int64_t)64), 256, 0, c->stream>>>(n, p0, nb, L, bad);
+        RCG_LAUNCH_CHECK(c);
+      }
+      chol_diag_kernel<<<1, 1024, 0, c->stream>>>(n, p0, nb, L, pivmax, pivot_rtol, bad);
+      RCG_LAUNCH_CHECK(c);
+      if (p0 + nb < n) {
+        const int trsm_smem = (int)(sizeof(double) * CHOL_NB * (CHOL_NB + CHOL_TRSM_ROWS));
+        RCG_CUDA(c, cudaFuncSetAttribute(chol_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem));
+        chol_trsm_kernel<<<(unsigned)ceil_div(n - p0 - nb, (int64_t)CHOL_TRSM_ROWS), CHOL_TRSM_ROWS, trsm_smem,
+                           c->stream>>>(n, p0, nb, L, bad);
+        RCG_LAUNCH_CHECK(c);
+      }
     }
   }
   long long hbad = -1;
@@ -299,8 +488,19 @@ int cholesky(Ctx* c, const double* G, int64_t n, double pivot_rtol, double* L, d
     // Linv lives outside the ctx scratch because gemm_tn reuses the scratch
     double* Linv = nullptr;
     RCG_CUDA(c, cudaMallocAsync((void**)&Linv, sizeof(double) * (size_t)n * n, c->stream));
-    trtri_lower_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, c->stream>>>(n, L, Linv);
-    RCG_LAUNCH_CHECK(c);
+    if (n <= CHOL_SMEM_MAX) {
+      trtri_lower_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, c->stream>>>(n, L, Linv);
+      RCG_LAUNCH_CHECK(c);
+    } else {
+      double* Lt = nullptr;
+      RCG_CUDA(c, cudaMallocAsync((void**)&Lt, sizeof(double) * (size_t)n * n, c->stream));
+      transpose_kernel<<<dim3((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32)), dim3(32, 8), 0, c->stream>>>(
+          n, L, Lt);
+      RCG_LAUNCH_CHECK(c);
+      trtri_warp_kernel<<<(unsigned)ceil_div(n * 32, (int64_t)256), 256, 0, c->stream>>>(n, Lt, Linv);
+      RCG_LAUNCH_CHECK(c);
+      cudaFreeAsync(Lt, c->stream);
+    }
     rc = gemm_tn(c, n, n, n, Linv, n, Linv, n, Ginv, 1);   // Ginv = Linv^T Linv
     cudaFreeAsync(Linv, c->stream);
     if (rc) return rc;

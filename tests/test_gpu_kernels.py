@@ -59,7 +59,7 @@ def test_diagonal_and_jacobi():
     np.testing.assert_array_equal(A.diagonal(), [2.0, 4.0])
 
 
-@pytest.mark.parametrize("n", [2, 3, 10, 50, 127, 200])
+@pytest.mark.parametrize("n", [2, 3, 10, 50, 127, 200, 700, 1601])
 def test_cholesky_matches_oracle(rng, n):
     G = problems.random_spd(n, rng)
     L = rcg.dense_cholesky(G)
@@ -75,7 +75,7 @@ def test_cholesky_kats():
         rcg.dense_cholesky(np.array([[1.0, 2.0], [0.0, 1.0]]))
 
 
-@pytest.mark.parametrize("n,bad", [(40, 20), (150, 97)])
+@pytest.mark.parametrize("n,bad", [(40, 20), (150, 97), (900, 640), (900, 64), (900, 899)])
 def test_cholesky_rank_deficient_column(rng, n, bad):
     # reference tests/test_core.py:136-146 (and the > 128 global-memory path)
     G = problems.random_spd(n, rng)
@@ -88,6 +88,24 @@ def test_cholesky_rank_deficient_column(rng, n, bad):
     with pytest.raises(orc.OracleRankDeficient) as eo:
         orc.dense_cholesky(0.5 * (G2 + G2.T), pivot_rtol=1e-12)
     assert eo.value.column == bad
+
+
+@pytest.mark.parametrize("n", [60, 300, 1200])
+def test_cholesky_inverse_blocked(rng, n):
+    """G^-1 = L^-T L^-1 as build_deflation forms it (small: per-column
+    substitution; n > 128: blocked factor + warp-per-column inverse)."""
+    import torch
+    from paper_1301_7530_b200 import _lib
+    G = problems.random_spd(n, rng, condition=1e4)
+    Gd = torch.from_numpy(np.ascontiguousarray(G)).cuda()
+    L = torch.empty_like(Gd)
+    Gi = torch.empty_like(Gd)
+    bad = _lib.C.c_int64(-1)
+    ctx = _lib.context()
+    ctx.check(ctx.lib.rcg_dense_cholesky(ctx.h, _lib.ptr(Gd), n, 1e-12, _lib.ptr(L), _lib.ptr(Gi),
+                                         _lib.C.byref(bad)), "cholesky")
+    Gih = Gi.cpu().numpy()
+    np.testing.assert_allclose(Gih, np.linalg.inv(G), rtol=0, atol=1e-9 * np.abs(np.linalg.inv(G)).max())
 
 
 def test_tridiag_eig_closed_form():
@@ -282,3 +300,15 @@ def test_dia3_tma_matches():
     np.testing.assert_allclose(t["alphas"], a["alphas"], rtol=1e-12)
     np.testing.assert_allclose([t["x_sum"], t["x_norm"], t["resid"]], [a["x_sum"], a["x_norm"], a["resid"]],
                                rtol=1e-9)
+
+
+@pytest.mark.parametrize("count,dtype", [(5_000_003, np.float64), (9_000_001, np.int32), (33_554_432 // 8, np.float64)])
+def test_pinned_staged_upload_is_exact(count, dtype):
+    """core.h2d (pinned-ring upload used for large CSR arrays) is a plain copy."""
+    from paper_1301_7530_b200 import core
+    rng = np.random.default_rng(count)
+    a = rng.standard_normal(count).astype(dtype) if dtype == np.float64 else \
+        rng.integers(-2 ** 31, 2 ** 31 - 1, count, dtype=np.int64).astype(np.int32)
+    d = core.h2d(a)
+    assert d.is_cuda and d.dtype == getattr(__import__("torch"), str(a.dtype))
+    np.testing.assert_array_equal(d.cpu().numpy(), a)
