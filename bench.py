@@ -405,7 +405,10 @@ def run_ours(args):
     ctx.set_profiling(True)
     k_prof, rec_prof, _ = seq.step()
     ctx.set_profiling(False)
-    stats = ctx.kernel_stats()
+    stats_all = ctx.kernel_stats()
+    phases = {k: {"seconds": round(v["seconds"], 6), "launches": v["launches"]} for k, v in stats_all.items()
+              if k in ("halo", "allreduce")}
+    stats = {k: v for k, v in stats_all.items() if k not in ("halo", "allreduce")}
     dom = max(stats, key=lambda kk: stats[kk]["seconds"])
     tot_k = sum(s["seconds"] for s in stats.values())
     peak, peak_src = peaks()
@@ -542,6 +545,8 @@ def run_ours(args):
             "per_system": {str(k): {"seconds": round(v[0], 4), "iterations": v[1]}
                            for k, v in sorted(per_system.items())},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "secondary": secondary,
+            "phases_profiled_step": ({"kernels_seconds": sum(s["seconds"] for s in stats.values()), **phases}
+                                     if world > 1 else None),
             "gpu_launches": launches, "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -176,7 +176,9 @@ enum rcg_kclass {
   RCG_K_COLREDUCE = 4, /* K4: reorth partial reduction                  */
   RCG_K_WUPDATE = 5,   /* K5: w = z + beta w - W c                      */
   RCG_K_ACTR = 6,      /* K2b: AC^T (M^-1 r), projector GEMV-T (n_c > 0) */
-  RCG_K_NUM = 7
+  RCG_K_HALO = 7,      /* sharded: ghost exchange of w_j (pack, NCCL send/recv, unpack) */
+  RCG_K_ALLREDUCE = 8, /* sharded: packed fp64 allreduces of the reduction slots */
+  RCG_K_NUM = 9
 };
 typedef struct {
   int64_t launches;

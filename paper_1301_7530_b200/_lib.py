@@ -65,7 +65,7 @@ class RcgKernelStat(C.Structure):
     _fields_ = [("launches", C.c_int64), ("seconds", C.c_double), ("bytes", C.c_double)]
 
 
-KCLASSES = ("spmv", "update", "coarse", "precond", "colreduce", "wupdate", "actr")
+KCLASSES = ("spmv", "update", "coarse", "precond", "colreduce", "wupdate", "actr", "halo", "allreduce")
 
 _vp = C.c_void_p
 _i64 = C.c_int64

@@ -8,6 +8,7 @@
 #include "comm.cuh"
 
 #include <dlfcn.h>
+#include <algorithm>
 #include <cstring>
 #include <condition_variable>
 #include <mutex>
@@ -177,8 +178,21 @@ static int loop_halo(Ctx* c, const rcg_halo* H, double* dst_col) {
   return RCG_OK;
 }
 
+// RCG_COMM_FORCE=1: issue NCCL collectives even on one rank (exercises the
+// NCCL calls, incl. their CUDA-graph capture, on a single GPU)
+static bool comm_force() {   // read per call: tests switch it within one process
+  const char* e = getenv("RCG_COMM_FORCE");
+  return e && atoi(e) != 0;
+}
+
+bool comm_graphable(const Ctx* c) {
+  const char* e = getenv("RCG_SHARDED_GRAPHS");
+  return !(e && atoi(e) == 0) && c->comm && !c->comm->loop;
+}
+
 int allreduce_sum(Ctx* c, double* buf, size_t count) {
-  if (!c->comm || c->comm->nranks <= 1 || count == 0) return RCG_OK;
+  if (!c->comm || count == 0) return RCG_OK;
+  if (c->comm->nranks <= 1 && !(comm_force() && !c->comm->loop && c->comm->comm)) return RCG_OK;
   if (c->comm->loop) return loop_allreduce(c, buf, count);
   RCG_NCCL(c, c->comm->api.allReduce(buf, buf, count, kNcclFloat64, kNcclSum, c->comm->comm, c->stream));
   return RCG_OK;
@@ -225,7 +239,48 @@ int halo_exchange(Ctx* c, const rcg_halo* H, ColSel src, const SolveState* st, d
   return RCG_OK;
 }
 
+__global__ void halo_unpack_kernel(int64_t n_ghost, int64_t n_local, const double* __restrict__ in, ColSel dst,
+                                   const SolveState* st) {
+  long long j = 0;
+  if (st) j = st->j;
+  double* d = dst.at(j) + n_local;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n_ghost; k += (int64_t)gridDim.x * blockDim.x)
+    d[k] = in[k];
+}
+
+int halo_prepare(Ctx* c, const rcg_halo* H) {
+  if (!H || H->n_ghost <= 0 || c->halo_recv_cap >= (size_t)H->n_ghost) return RCG_OK;
+  RCG_CUDA(c, cudaStreamSynchronize(c->stream));   // the old buffer may still be read
+  if (c->halo_recv) cudaFree(c->halo_recv);
+  c->halo_recv = nullptr;
+  c->halo_recv_cap = 0;
+  RCG_CUDA(c, cudaMalloc((void**)&c->halo_recv, sizeof(double) * (size_t)H->n_ghost));
+  c->halo_recv_cap = (size_t)H->n_ghost;
+  return RCG_OK;
+}
+
+int halo_exchange_dev(Ctx* c, const rcg_halo* H, ColSel src, const SolveState* st, ColSel dst) {
+  if (!H || !c->comm || c->comm->nranks <= 1) return RCG_OK;
+  if (H->n_ghost > (int64_t)c->halo_recv_cap)
+    return set_error(c, RCG_ERR_CONTRACT, "halo staging not prepared (halo_prepare before the solve loop)");
+  // received ghosts land at halo_recv + recv_off[q] (the exchange's "column"
+  // is halo_recv - n_local), then move into the destination column at j
+  int rc = halo_exchange(c, H, src, st, c->halo_recv - H->n_local);
+  if (rc) return rc;
+  if (H->n_ghost > 0) {
+    const int g = (int)std::min<int64_t>(ceil_div(H->n_ghost, (int64_t)kThreads), 2 * c->num_sms);
+    halo_unpack_kernel<<<g, kThreads, 0, c->stream>>>(H->n_ghost, H->n_local, c->halo_recv, dst, st);
+    RCG_LAUNCH_CHECK(c);
+  }
+  return RCG_OK;
+}
+
 void comm_free(Ctx* c) {
+  if (c->halo_recv) {
+    cudaFree(c->halo_recv);
+    c->halo_recv = nullptr;
+    c->halo_recv_cap = 0;
+  }
   if (c->comm) {
     if (!c->comm->loop && c->comm->comm && c->comm->api.commDestroy) c->comm->api.commDestroy(c->comm->comm);
     delete c->comm;

@@ -8,5 +8,13 @@ int allreduce_sum(Ctx* c, double* buf, size_t count);
 // pack src[send_idx] and exchange with every peer; received ghosts land at
 // dst_col + n_local + recv_off[q] (no-op without a communicator)
 int halo_exchange(Ctx* c, const rcg_halo* H, ColSel src, const SolveState* st, double* dst_col);
+// solve-loop variant with fixed addresses (CUDA-graph capturable with NCCL):
+// pack src.at(j), receive into the ctx staging buffer, unpack into
+// dst.at(j)[n_local + ...] with j read from st on the device
+// allocate the ctx staging buffer for H's ghosts (outside any graph capture)
+int halo_prepare(Ctx* c, const rcg_halo* H);
+int halo_exchange_dev(Ctx* c, const rcg_halo* H, ColSel src, const SolveState* st, ColSel dst);
+// whether solve-loop batches of a sharded solve may be captured in a graph
+bool comm_graphable(const Ctx* c);
 void comm_free(Ctx* c);
 }  // namespace rcg

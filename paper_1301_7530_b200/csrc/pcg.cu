@@ -42,6 +42,12 @@ namespace rcg {
 #define RCG_GEMV_UNROLL 2
 #endif
 constexpr int kGemvUnroll = RCG_GEMV_UNROLL;
+#ifndef RCG_PRE_FENCE
+#define RCG_PRE_FENCE 1   // A/B r02m: K3 6.60 -> 6.73 TB/s in-solve (config 3)
+#endif
+#ifndef RCG_WU_KB
+#define RCG_WU_KB 2     // K5 columns per explicit load batch (x RPT/2 128-bit loads)
+#endif
 #ifndef RCG_ACTR_PIPE
 #define RCG_ACTR_PIPE 1
 #endif
@@ -157,13 +163,19 @@ __device__ __forceinline__ void gemv_t_tile(const double* __restrict__ base, int
         // otherwise interleaves them with the FMAs and keeps only ~4 loads in
         // flight: tools/k3_layout_bench.cu, 6.96 -> 7.12 TB/s at config 3).
         // Accumulation order per column is unchanged (step p, then p + 32).
-        int64_t pi = p_begin + lane;
-        for (; pi + 32 < p_end; pi += 64) {
+        // warp-uniform trip count (the scheduling fence below needs every
+        // lane): full double steps while 64 pairs remain, then single steps
+        int64_t base = p_begin;
+        for (; base + 64 <= p_end; base += 64) {
+          const int64_t pi = base + lane;
           double2 va[CG], vb[CG];
 #pragma unroll
           for (int c = 0; c < CG; ++c) va[c] = __ldcs(reinterpret_cast<const double2*>(cols + c * ld) + pi);
 #pragma unroll
           for (int c = 0; c < CG; ++c) vb[c] = __ldcs(reinterpret_cast<const double2*>(cols + c * ld) + pi + 32);
+#if RCG_PRE_FENCE
+          __syncwarp();   // scheduling fence: all 2 CG loads issue before the first FMA
+#endif
           const double2 x0a = *reinterpret_cast<const double2*>(v0 + 2 * pi);
           const double2 x0b = *reinterpret_cast<const double2*>(v0 + 2 * (pi + 32));
           double2 x1a = make_double2(0.0, 0.0), x1b = make_double2(0.0, 0.0);
@@ -179,15 +191,15 @@ __device__ __forceinline__ void gemv_t_tile(const double* __restrict__ base, int
             if (NV == 2) a1[c] = fma(vb[c].y, x1b.y, fma(vb[c].x, x1b.x, a1[c]));
           }
         }
-        if (pi < p_end) {
+        for (int64_t pi = base + lane; pi < p_end; pi += 32) {
           const double2 x0 = *reinterpret_cast<const double2*>(v0 + 2 * pi);
           double2 x1 = make_double2(0.0, 0.0);
           if (NV == 2) x1 = *reinterpret_cast<const double2*>(v1 + 2 * pi);
 #pragma unroll
           for (int c = 0; c < CG; ++c) {
             const double2 v = __ldcs(reinterpret_cast<const double2*>(cols + c * ld) + pi);
-            a0[c] += v.x * x0.x + v.y * x0.y;
-            if (NV == 2) a1[c] += v.x * x1.x + v.y * x1.y;
+            a0[c] = fma(v.y, x0.y, fma(v.x, x0.x, a0[c]));
+            if (NV == 2) a1[c] = fma(v.y, x1.y, fma(v.x, x1.x, a1[c]));
           }
         }
       } else if (kc == CG) {
@@ -643,6 +655,11 @@ colreduce_kernel(const IterArgs* __restrict__ ap) {
     }
     __syncthreads();
   }
+  // zero the slots past 2(j+1) up to the history capacity: a sharded batch
+  // allreduces the whole capacity (one width per captured graph)
+  for (int64_t q = Q + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < a.reo_stride;
+       q += (int64_t)gridDim.x * blockDim.x)
+    a.sums[a.rz_off + 1 + q] = 0.0;
 }
 
 // ---------------------------------------------------------------------------
@@ -989,8 +1006,17 @@ wupdate_plain_kernel(const IterArgs* __restrict__ ap) {
   }
 }
 
+// Rows of a block: thread t owns the row pairs (r0 + 2 (t + q kThreads), +1),
+// q < RPT / 2, so every W load is one 128-bit access; acc[2q + e] is row
+// r0 + 2 (t + q kThreads) + e.  Each row's W c sum keeps the reference's
+// column order (k ascending, one rounding per FMA).
 template <int RPT>
-__global__ void __launch_bounds__(kThreads)
+__device__ __forceinline__ int64_t wu_row(int64_t r0, int q2) {
+  return r0 + 2 * ((int64_t)threadIdx.x + (q2 >> 1) * kThreads) + (q2 & 1);
+}
+
+template <int RPT>
+__global__ void __launch_bounds__(kThreads, 3)
 wupdate_kernel(const IterArgs* __restrict__ ap) {
   pdl_wait();
   const IterArgs& a = *ap;
@@ -1029,16 +1055,40 @@ wupdate_kernel(const IterArgs* __restrict__ ap) {
       }
       __syncthreads();
       // reorth implies a stored W history (ColSel mod == 0): column k at base + k ld
-      const double* col0 = a.W.base + (k0 + a.W.shift) * a.W.ld + r0 + threadIdx.x;
+      const double* col0 = a.W.base + (k0 + a.W.shift) * a.W.ld + r0;
       const int64_t ldw = a.W.ld;
+      constexpr int PPT = RPT / 2, KB = RCG_WU_KB;
       if (r0 + (int64_t)kThreads * RPT <= a.n) {
-        // full row block: RPT x 4 independent loads in flight per thread
-#pragma unroll 4
-        for (long long k = 0; k < kn; ++k) {
-          const double* col = col0 + k * ldw;
+        // full row block: the 128-bit loads of KB columns x PPT row pairs are
+        // issued before their FMAs (at the 80-register budget the compiler
+        // otherwise interleaves them and keeps ~7 loads in flight)
+        long long k = 0;
+        for (; k + KB <= kn; k += KB) {
+          double2 v[KB][PPT];
+#pragma unroll
+          for (int u = 0; u < KB; ++u)
+#pragma unroll
+            for (int q = 0; q < PPT; ++q)
+              v[u][q] = __ldcs(reinterpret_cast<const double2*>(col0 + (k + u) * ldw) + threadIdx.x + q * kThreads);
+          __syncwarp();   // scheduling fence: every load of the batch issues before the first FMA
+#pragma unroll
+          for (int u = 0; u < KB; ++u) {
+            const double ck = cp[k + u];
+#pragma unroll
+            for (int q = 0; q < PPT; ++q) {
+              acc[2 * q] = fma(v[u][q].x, ck, acc[2 * q]);
+              acc[2 * q + 1] = fma(v[u][q].y, ck, acc[2 * q + 1]);
+            }
+          }
+        }
+        for (; k < kn; ++k) {
           const double ck = cp[k];
 #pragma unroll
-          for (int q = 0; q < RPT; ++q) acc[q] += __ldcs(col + q * kThreads) * ck;
+          for (int q = 0; q < PPT; ++q) {
+            const double2 v = __ldcs(reinterpret_cast<const double2*>(col0 + k * ldw) + threadIdx.x + q * kThreads);
+            acc[2 * q] = fma(v.x, ck, acc[2 * q]);
+            acc[2 * q + 1] = fma(v.y, ck, acc[2 * q + 1]);
+          }
         }
       } else {
 #pragma unroll 4
@@ -1046,8 +1096,10 @@ wupdate_kernel(const IterArgs* __restrict__ ap) {
           const double* col = col0 + k * ldw;
           const double ck = cp[k];
 #pragma unroll
-          for (int q = 0; q < RPT; ++q)
-            if (r0 + threadIdx.x + q * kThreads < a.n) acc[q] += col[q * kThreads] * ck;
+          for (int q2 = 0; q2 < RPT; ++q2) {
+            const int64_t i = wu_row<RPT>(r0, q2);
+            if (i < a.n) acc[q2] = fma(col[i - r0], ck, acc[q2]);
+          }
         }
       }
     }
@@ -1058,7 +1110,7 @@ wupdate_kernel(const IterArgs* __restrict__ ap) {
     // them in split order (deterministic) and finishes the rows
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
-      const int64_t i = r0 + threadIdx.x + q * kThreads;
+      const int64_t i = wu_row<RPT>(r0, q);
       if (i < a.n) a.part_wu[(int64_t)split * a.n + i] = acc[q];
     }
     __syncthreads();  // + thread-0 fence (cumulative), see arrive_last
@@ -1075,7 +1127,7 @@ wupdate_kernel(const IterArgs* __restrict__ ap) {
       __threadfence();
 #pragma unroll
       for (int q = 0; q < RPT; ++q) {
-        const int64_t i = r0 + threadIdx.x + q * kThreads;
+        const int64_t i = wu_row<RPT>(r0, q);
         double t = 0.0;
         if (i < a.n)
           for (int sp = 0; sp < S; ++sp) t += __ldcg(a.part_wu + (int64_t)sp * a.n + i);
@@ -1089,7 +1141,7 @@ wupdate_kernel(const IterArgs* __restrict__ ap) {
     double* wn = a.W.at(j + 1);
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
-      const int64_t i = r0 + threadIdx.x + q * kThreads;
+      const int64_t i = wu_row<RPT>(r0, q);
       if (i < a.n) {
         double v = __dadd_rn(z[i], __dmul_rn(beta, wo[i]));   // w = z + beta w
         if (a.reorth) v = __dsub_rn(v, acc[q]);                // w -= W c'
@@ -1577,6 +1629,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     return RCG_OK;
   };
   if ((rc = ensure_sums())) return fail(rc);
+  if (H && (rc = halo_prepare(c, H))) return fail(rc);    // staging for the loop's graph-capturable exchange
 
   if (!c->dargs && cudaMalloc(&c->dargs, 4096) != cudaSuccess) return fail(set_error(c, RCG_ERR_OOM, "args"));
   static_assert(sizeof(IterArgs) <= 4096, "IterArgs too large");
@@ -1775,23 +1828,34 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
           ? 8.0 * (double)A->nnz + 4.0 * (double)A->nnz / 9.0 + 4.0 * (double)(n / 3 + 1) + 16.0 * (double)n
           : 12.0 * (double)A->nnz + (A->row_offsets_64 ? 8.0 : 4.0) * (double)(n + 1) + 16.0 * (double)n;
   static const int use_graphs = env_int("RCG_GRAPHS", 1);
+  const double halo_bytes = H ? 8.0 * ((double)H->send_off[H->nranks] + (double)H->n_ghost) : 0.0;
+  bool direct_now = false;   // set by launch_batch: profile the collectives too
+  auto allreduce_p = [&](double* buf, size_t count, int64_t jj) -> int {
+    if (!H) return RCG_OK;
+    if (direct_now) prof_begin(c, RCG_K_ALLREDUCE, 8.0 * (double)count, jj);
+    const int r = allreduce_sum(c, buf, count);
+    if (direct_now) prof_end(c);
+    return r;
+  };
   const int cr_grid = 2 * c->num_sms;
   // queue B iterations; `direct` allows the host-side per-iteration work
   // (profiling events, halo exchanges with jj-dependent addresses)
   auto launch_batch = [&](int64_t B, int64_t it0, bool direct) -> int {
     int rc2;
+    direct_now = direct;
     for (int64_t q = 0; q < B; ++q) {
       const int64_t jj = it0 + q;  // the device-side j unless the solve already stopped
       const double nd = (double)n, js = (double)(jj + 1);
-      if (H && direct) {  // ghosts of w_j from the neighbouring slabs
-        double* wcol = gW.ptr + (storeW ? jj : jj % 2) * ld;
-        if ((rc2 = halo_exchange(c, H, a.W, st, wcol))) return rc2;
+      if (H) {  // ghosts of w_j from the neighbouring slabs (column at device j: graph-capturable)
+        if (direct) prof_begin(c, RCG_K_HALO, halo_bytes, jj);
+        if ((rc2 = halo_exchange_dev(c, H, a.W, st, a.W))) return rc2;
+        if (direct) prof_end(c);
       }
       // algorithmic bytes per launch (each operand touched once)
       if (direct) prof_begin(c, RCG_K_SPMV, bytes_spmv, jj);
       if ((rc2 = launch_spmv_ind(c, A, &dargs->spmv))) return rc2;
       if (direct) prof_end(c);
-      if ((rc2 = allreduce_h(H, c, gSum.ptr, 1))) return rc2;
+      if ((rc2 = allreduce_p(gSum.ptr, 1, jj))) return rc2;
       if (direct) prof_begin(c, RCG_K_UPDATE, 8.0 * nd * (6 + (store ? 1 : 0)), jj);
       RCG_CUDA(c, launch_k(update_kernel, dim3(nbu_l), dim3(kThreads), 0, c->stream, (const IterArgs*)dargs, 0));
       c->launches++;
@@ -1803,7 +1867,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
         c->launches++;
         if (direct) prof_end(c);
       }
-      if ((rc2 = allreduce_h(H, c, gSum.ptr + 1, (size_t)(1 + n_c)))) return rc2;
+      if ((rc2 = allreduce_p(gSum.ptr + 1, (size_t)(1 + n_c), jj))) return rc2;
       if (n_c > NC_INLINE) {
         if (direct) prof_begin(c, RCG_K_COARSE, 8.0 * (double)n_c * (double)n_c, jj);
         if ((rc2 = launch_coarse(1))) return rc2;
@@ -1819,8 +1883,10 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
         c->launches++;
         if (direct) prof_end(c);
       }
-      // one packed allreduce: (r, z) and the 2(j+1) reorth dot products
-      if ((rc2 = allreduce_h(H, c, gSum.ptr + a.rz_off, (size_t)(1 + (reorth ? 2 * (jj + 1) : 0))))) return rc2;
+      // one packed allreduce: (r, z) and the reorth dot products, over the
+      // history capacity (fixed between regrows, so the graph replays it;
+      // colreduce zeroes the slots past 2(j+1))
+      if ((rc2 = allreduce_p(gSum.ptr + a.rz_off, (size_t)(1 + (reorth ? a.reo_stride : 0)), jj))) return rc2;
       if (direct) prof_begin(c, RCG_K_WUPDATE, 8.0 * nd * (3 + (reorth ? js : 0.0)), jj);
       if (!reorth)
         RCG_CUDA(c, launch_k(wupdate_plain_kernel<8>, dim3(wu_plain_grid), dim3(kThreads), 0, c->stream,
@@ -1862,7 +1928,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
       if ((rc = ensure_sums())) return fail(rc);
       RCG_CUDA_F(refresh());
     }
-    const bool graph_ok = use_graphs && !c->profiling && !H;
+    const bool graph_ok = use_graphs && !c->profiling && (!H || comm_graphable(c));
     if (small && !c->profiling) {
       long long Bl = (long long)B;
       const IterArgs* ap = dargs;
@@ -1873,10 +1939,11 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     } else if (graph_ok) {
       // one graph per (shape, batch size): parameters are all device-resident
       char key[256];
-      snprintf(key, sizeof(key), "%p|%lld|%d|%d|%d|%d|%zu|%zu|%d|%d|%lld|%d|%d", (void*)pre, (long long)n,
+      snprintf(key, sizeof(key), "%p|%lld|%d|%d|%d|%d|%zu|%zu|%d|%d|%lld|%d|%d|%p|%lld", (void*)pre, (long long)n,
                spmv_width(A), nbs, nb, nbu, smem_upd, smem_pre, reorth ? 1 : 0, n_c > NC_INLINE ? 1 : 0,
                (long long)B, A->block + 100 * A->bsr_slice + 10000 * (A->dia_count * 4 + A->dia_block),
-               A->row_offsets_64 + 2 * (int)ceil_div(n_c, 8));
+               A->row_offsets_64 + 2 * (int)ceil_div(n_c, 8), (const void*)H,
+               (long long)(H ? reo_cols() : 0));   // sharded: halo plan and allreduce width
       cudaGraphExec_t exec = nullptr;
       auto gi = c->graphs.find(key);
       if (gi != c->graphs.end()) {

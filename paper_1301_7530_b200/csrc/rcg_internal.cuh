@@ -71,6 +71,8 @@ struct Ctx {
   std::shared_ptr<VmmPool> vpool;        // whole mapped history ranges kept across solves
   std::map<int64_t, int64_t> m_hint;     // n -> iterations of the last solve
   Comm* comm = nullptr;                  // NCCL communicator (sharded runs)
+  double* halo_recv = nullptr;           // received ghosts, unpacked into the column at device j
+  size_t halo_recv_cap = 0;
   void* dargs = nullptr;                 // device-resident solve arguments (graph replay)
   cudaStream_t capture_stream = nullptr; // private stream for graph capture
   struct GraphEntry {
