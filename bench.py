@@ -362,13 +362,13 @@ def run_ours(args):
     # sequence's time is their sum; the process's very first step is cold)
     per_system = {}
 
-    def note(k, it, ev):
-        per_system[k] = (ev[0].elapsed_time(ev[1]) * 1e-3, it)
+    def note(k, rec, ev):
+        per_system[k] = (ev[0].elapsed_time(ev[1]) * 1e-3, rec.iterations, rec.n_c_before)
 
     for _ in range(args.warmup):
         k, rec, ev = timed_step()
         torch.cuda.synchronize()
-        note(k, rec.iterations, ev)
+        note(k, rec, ev)
 
     ctx = _lib.context()
     t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -382,21 +382,21 @@ def run_ours(args):
         for _ in range(args.steps):
             k, rec, ev = timed_step()
             iters += rec.iterations
-            step_events.append((k, rec.iterations, ev))
+            step_events.append((k, rec, ev))
         t1e.record(stream)
         torch.cuda.synchronize()
         barrier()
     launches = _lib.total_launches() - l0
     sec = max_over_ranks(t0e.elapsed_time(t1e) * 1e-3)
     value = (iters if sharded else world * iters) / sec
-    timed_systems = [(k, it) for k, it, _ in step_events]
-    for k, it, ev in step_events:
-        note(k, it, ev)
+    timed_systems = [(k, rec.iterations) for k, rec, _ in step_events]
+    for k, rec, ev in step_events:
+        note(k, rec, ev)
     # complete one full sequence's per-system times (systems not run yet)
     while len(per_system) < count:
         k, rec, ev = timed_step()
         torch.cuda.synchronize()
-        note(k, rec.iterations, ev)
+        note(k, rec, ev)
     seq_seconds = max_over_ranks(sum(v[0] for v in per_system.values()))
     seq_iters = sum(v[1] for v in per_system.values())
 
@@ -542,7 +542,7 @@ def run_ours(args):
             "timed_systems": timed_systems, "iterations_timed": iters,
             "sequence_seconds": seq_seconds, "sequence_iterations": seq_iters,
             "sequence_iters_per_s": seq_iters / seq_seconds if seq_seconds else None,
-            "per_system": {str(k): {"seconds": round(v[0], 4), "iterations": v[1]}
+            "per_system": {str(k): {"seconds": round(v[0], 4), "iterations": v[1], "n_c_before": v[2]}
                            for k, v in sorted(per_system.items())},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "secondary": secondary,
             "phases_profiled_step": ({"kernels_seconds": sum(s["seconds"] for s in stats.values()), **phases}
