@@ -437,6 +437,30 @@ __host__ __device__ __forceinline__ int64_t dia_q_stride(int64_t nbr, int BB) {
 #define RCG_DIA3_MINB 2   // 128 registers: 2 CTAs/SM with 4 blocks (48 loads) in flight per thread
 #endif
 
+// L2 eviction hints for the DIA stream (RCG_DIA_HINT): an upper block U_d(p)
+// is read again ~o block rows later as the lower block of row p + o, and every
+// x entry feeds all the rows of its stencil, so the first touches are kept
+// (evict_last) and the second touch of a value block is released
+// (evict_first).  createpolicy / ld.global.L2::cache_hint (sm_80+).
+#ifndef RCG_DIA_HINT
+#define RCG_DIA_HINT 0
+#endif
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ld_nc_hint(const double* ptr, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(ptr), "l"(pol));
+  return v;
+}
+
 // ND > 0: the diagonal count is a compile-time constant (5/7-point: 3/4
 // upper diagonals, Q1 27-point blocks: 14), so both diagonal loops unroll
 // fully and every value / x load of a row is independent and in flight at
@@ -463,6 +487,11 @@ __device__ __forceinline__ bool dia_body(int64_t nbr, int nd_rt, const int64_t* 
   // (b = 3 only: 833 vs 869 us at 160^3; the scalar stencil prefers the
   // plain per-thread sweep, 162 vs 172 us at 256^3)
   const int lane = B == 3 ? (int)(threadIdx.x & 31) : 0;
+  uint64_t pol_keep = 0, pol_drop = 0;
+  if (RCG_DIA_HINT) {
+    pol_keep = l2_policy_last();
+    pol_drop = l2_policy_first();
+  }
   for (int64_t pw = (int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; pw < nbr;
        pw += (int64_t)gridDim.x * blockDim.x) {
     const bool act = pw + lane < nbr;
@@ -492,12 +521,19 @@ __device__ __forceinline__ bool dia_body(int64_t nbr, int nd_rt, const int64_t* 
         ok[k] = t < nt && (lower[k] ? p >= o : p + o < nbr);
         const int64_t ub = lower[k] ? (ok[k] ? p - o : 0) : p;        // block row of the stored U_d
         const int64_t xb = lower[k] ? ub : (ok[k] ? p + o : p);       // block column
-#pragma unroll
-        for (int jj = 0; jj < B; ++jj) xv[k][jj] = __ldg(x + B * xb + jj);
         const double* __restrict__ u = U + dia_at(d, 0, ub, nbr, BB);
         const int64_t qs = dia_q_stride(nbr, BB);
+        if (RCG_DIA_HINT) {
 #pragma unroll
-        for (int q = 0; q < BB; ++q) v[k][q] = __ldg(u + q * qs);
+          for (int jj = 0; jj < B; ++jj) xv[k][jj] = ld_nc_hint(x + B * xb + jj, pol_keep);
+#pragma unroll
+          for (int q = 0; q < BB; ++q) v[k][q] = ld_nc_hint(u + q * qs, lower[k] ? pol_drop : pol_keep);
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < B; ++jj) xv[k][jj] = __ldg(x + B * xb + jj);
+#pragma unroll
+          for (int q = 0; q < BB; ++q) v[k][q] = __ldg(u + q * qs);
+        }
       }
 #pragma unroll
       for (int k = 0; k < K; ++k) {
