@@ -24,6 +24,15 @@
 #ifndef RCG_SPMV_MINB
 #define RCG_SPMV_MINB 4
 #endif
+#ifndef RCG_CSR_PAIRS_V2
+#define RCG_CSR_PAIRS_V2 5
+#endif
+#ifndef RCG_CSR_PAIRS_V4
+#define RCG_CSR_PAIRS_V4 7
+#endif
+#ifndef RCG_CSR_PAIRS_V8
+#define RCG_CSR_PAIRS_V8 0
+#endif
 #ifndef RCG_SPMV_U8
 #define RCG_SPMV_U8 12
 #endif
@@ -78,15 +87,20 @@ __device__ __forceinline__ void spmv_body(int64_t n, const RO* __restrict__ ro, 
     }
     double s = 0.0;
     const bool fast = __all_sync(0xffffffffu, (re - rs) <= (int64_t)U * V);
-    if (V >= 2 && fast) {
-      // 128-bit value / 64-bit index loads: the row's entries as aligned pairs
-      // (2p, 2p+1), lane `sub` takes pairs ps + sub, ps + sub + V, ...; the
-      // entries of a boundary pair outside [rs, re) are masked (no gather).
-      // A pair that would read past nnz falls back to one scalar load.
-      constexpr int UP = U / 2 + 1;            // <= U V entries span <= U V / 2 + 1 pairs
-      const int64_t ps = rs >> 1, pe = (re + 1) >> 1;
-      int2 c[UP];
-      double2 v[UP];
+    // 128-bit value / 64-bit index loads: the row's entries as aligned pairs
+    // (2p, 2p+1), lane `sub` takes pairs ps + sub, ps + sub + V, ...; the
+    // entries of a boundary pair outside [rs, re) are masked (no gather).  A
+    // pair that would read past nnz falls back to one scalar load.  UP pairs
+    // per lane (RCG_CSR_PAIRS_V*, 0 = scalar loads): measured per V because
+    // the pair registers compete with the loads in flight (V = 8 at UP = 7
+    // spilled: 162 -> 247 us at Q1 64^3)
+    constexpr int UP = V == 2 ? RCG_CSR_PAIRS_V2 : (V == 4 ? RCG_CSR_PAIRS_V4 : (V == 8 ? RCG_CSR_PAIRS_V8 : 0));
+    const int64_t ps = rs >> 1, pe = (re + 1) >> 1;
+    const bool fastp = UP > 0 && __all_sync(0xffffffffu, (pe - ps) <= (int64_t)UP * V);
+    if (UP > 0 && fastp) {
+      constexpr int UPA = UP > 0 ? UP : 1;
+      int2 c[UPA];
+      double2 v[UPA];
 #pragma unroll
       for (int u = 0; u < UP; ++u) {
         const int64_t p = ps + sub + (int64_t)u * V;

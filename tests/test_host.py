@@ -220,3 +220,52 @@ def test_reference_bridge_rebinds_every_seam(tmp_path):
         sys.path.remove(src)
         for k in [k for k in sys.modules if k == "recycg" or k.startswith("recycg.")]:
             del sys.modules[k]
+
+
+def _reference_src(tmp_path):
+    import zipfile
+    zp = REPO / "oracle" / "_ref" / "recycg_ref.zip"
+    if Path("/root/reference/pkg/src/recycg").is_dir():
+        return "/root/reference/pkg/src"
+    if zp.exists():
+        with zipfile.ZipFile(zp) as z:
+            z.extractall(tmp_path)
+        return str(tmp_path / "src")
+    pytest.skip("reference not available")
+
+
+def test_report_writers_match_reference_schema(tmp_path):
+    """runs.csv / summary.json / curve files byte-identical to the reference
+    CLI's writers (cli.py:181-244) for the same records."""
+    import importlib
+    from paper_1301_7530_b200 import report
+    src = _reference_src(tmp_path)
+    sys.path.insert(0, src)
+    try:
+        cli = importlib.import_module("recycg.cli")
+        rng = np.random.default_rng(5)
+        runs = []
+        for name, pc, tol, seed in [("srks14", "jacobi", 1e-3, 0), ("trks", "identity", 1e-6, 3)]:
+            rep = rcg.SequenceReport()
+            for k in range(4):
+                rep.records.append(rcg.SystemRecord(k, int(rng.integers(10, 500)), int(rng.integers(0, 90)),
+                                                    int(rng.integers(0, 9)), float(rng.uniform(0, 2)),
+                                                    float(rng.uniform(0, 1)), float(rng.uniform(1e-9, 1e-3)),
+                                                    bool(k != 2 or name == "trks")))
+            runs.append(report.RunResult(name, pc, tol, seed, rep))
+        ours = tmp_path / "ours"
+        report.write_report(ours, runs)
+        theirs = tmp_path / "theirs"
+        none = cli.RecycleStrategy("none")   # no final bases: the reference's overlap file is skipped
+        ref_runs = [cli.RunResult(r.name, none, r.preconditioner, r.tol, r.seed, r.report) for r in runs]
+        cfg = type("Cfg", (), {})()
+        cli._write_outputs(cfg, ref_runs, theirs)
+        names = sorted(p.name for p in theirs.iterdir())
+        assert names == sorted(p.name for p in ours.iterdir())
+        for nm in names:
+            assert (ours / nm).read_text() == (theirs / nm).read_text(), nm
+        assert report.CSV_HEADER == cli.CSV_HEADER
+    finally:
+        sys.path.remove(src)
+        for k in [k for k in sys.modules if k == "recycg" or k.startswith("recycg.")]:
+            del sys.modules[k]

@@ -1,0 +1,5 @@
+for v in P0 P5 P5m3 P4m3 P0m3; do
+  for V in 8 4; do
+    RCG_SPMV_V=$V RCG_LIB=paper_1301_7530_b200/ab/$v/librcg.so python tools/spmv_bench.py elast64 csr 2>&1 | sed "s/^/$v /"
+  done
+done
