@@ -31,7 +31,7 @@
 #define RCG_CSR_PAIRS_V4 7
 #endif
 #ifndef RCG_CSR_PAIRS_V8
-#define RCG_CSR_PAIRS_V8 0
+#define RCG_CSR_PAIRS_V8 5
 #endif
 #ifndef RCG_SPMV_U8
 #define RCG_SPMV_U8 12
