@@ -451,31 +451,43 @@ __host__ __device__ __forceinline__ int64_t dia_q_stride(int64_t nbr, int BB) {
 #define RCG_DIA3_MINB 2   // 128 registers: 2 CTAs/SM with 4 blocks (48 loads) in flight per thread
 #endif
 
-// L2 eviction hints for the DIA stream (RCG_DIA_HINT): an upper block U_d(p)
-// is read again ~o block rows later as the lower block of row p + o, and every
-// x entry feeds all the rows of its stencil, so the first touches are kept
-// (evict_last) and the second touch of a value block is released
-// (evict_first).  createpolicy / ld.global.L2::cache_hint (sm_80+).
-#ifndef RCG_DIA_HINT
-#define RCG_DIA_HINT 0
-#endif
 #ifndef RCG_DIA_FAST
 #define RCG_DIA_FAST 1   // predicate-free body for interior rows
 #endif
-__device__ __forceinline__ uint64_t l2_policy_last() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
+
+// Term order of a row sum in the interior-row body.  RCG_DIA3_ORDER=0:
+// ascending block column (lower d = ND-1..1, diagonal, upper d = 1..ND-1), the
+// CSR order.  RCG_DIA3_ORDER=1 (default; 3x3 blocks on 14 diagonals, i.e.
+// Q1 on a structured grid): the nine far diagonals (o about one grid plane)
+// first, each as the pair (lower d, upper d), then the near ones in column
+// order.  A far block U_d(q) is read twice, by row q + o_d as its lower
+// (transposed) block and by row q as its upper block; both rows are in flight
+// in the same sweep of the grid.  In column order the lower use sits in the
+// first load batch of its row and the upper use in the last, ~10 us apart,
+// and by then the line has left L2: ncu at 96^3 shows 1,179 MB of DRAM reads
+// for 925 MB of distinct bytes (+27%; +13% at 64^3), and the kernel already
+// runs at 6.3 TB/s of DRAM traffic.  Paired, both uses fall in the same phase
+// of the two rows: 955 MB (traffic / algorithmic 1.025), 187 -> 152-163 us at
+// 96^3 (5.1 -> 5.9-6.3 TB/s), 59.6 -> 51.3 us at 64^3
+// (profiles/r02y_dia3_order_ab.log).  The order is fixed per row, so results
+// stay reproducible; they differ from the CSR order at rounding level.
+// (Measured and dropped on the way, same log family: a bulk or per-line L2
+// prefetch of the row's upper runs at row start doubles the fetches of the
+// near diagonals instead, 241 us / 1,507 MB; L2 evict_last on the first
+// touch of a far block and evict_first on the second helps less than the
+// reorder, 178 us / 1,084 MB, and hurts on top of it, 175 us.)
+#ifndef RCG_DIA3_ORDER
+#define RCG_DIA3_ORDER 1
+#endif
+template <int B, int ND>
+__host__ __device__ constexpr bool dia_term_lower(int t) {
+  if (RCG_DIA3_ORDER == 1 && B == 3 && ND == 14) return t < 18 ? (t % 2 == 0) : t < 22;
+  return t < ND - 1;
 }
-__device__ __forceinline__ uint64_t l2_policy_first() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ double ld_nc_hint(const double* ptr, uint64_t pol) {
-  double v;
-  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(ptr), "l"(pol));
-  return v;
+template <int B, int ND>
+__host__ __device__ constexpr int dia_term_diag(int t) {
+  if (RCG_DIA3_ORDER == 1 && B == 3 && ND == 14) return t < 18 ? 13 - t / 2 : (t < 22 ? 22 - t : t - 22);
+  return t < ND - 1 ? ND - 1 - t : t - (ND - 1);
 }
 
 // ND > 0: the diagonal count is a compile-time constant (5/7-point: 3/4
@@ -504,11 +516,6 @@ __device__ __forceinline__ bool dia_body(int64_t nbr, int nd_rt, const int64_t* 
   // (b = 3 only: 833 vs 869 us at 160^3; the scalar stencil prefers the
   // plain per-thread sweep, 162 vs 172 us at 256^3)
   const int lane = B == 3 ? (int)(threadIdx.x & 31) : 0;
-  uint64_t pol_keep = 0, pol_drop = 0;
-  if (RCG_DIA_HINT) {
-    pol_keep = l2_policy_last();
-    pol_drop = l2_policy_first();
-  }
   for (int64_t pw = (int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; pw < nbr;
        pw += (int64_t)gridDim.x * blockDim.x) {
     const bool act = pw + lane < nbr;
@@ -538,8 +545,8 @@ __device__ __forceinline__ bool dia_body(int64_t nbr, int nd_rt, const int64_t* 
         for (int k = 0; k < K; ++k) {
           const int t = t0 + k;
           if (t >= 2 * ND - 1) break;
-          const bool lower = t < ND - 1;
-          const int d = lower ? ND - 1 - t : t - (ND - 1);
+          const bool lower = dia_term_lower<B, ND>(t);
+          const int d = dia_term_diag<B, ND>(t);
           const int64_t o = offs[d];
           const int64_t ub = lower ? p - o : p;
           const int64_t xb = lower ? ub : p + o;
@@ -554,8 +561,8 @@ __device__ __forceinline__ bool dia_body(int64_t nbr, int nd_rt, const int64_t* 
         for (int k = 0; k < K; ++k) {
           const int t = t0 + k;
           if (t >= 2 * ND - 1) break;
-          const bool lower = t < ND - 1;
-          if (t == ND - 1) {
+          const bool lower = dia_term_lower<B, ND>(t);
+          if (dia_term_diag<B, ND>(t) == 0) {
 #pragma unroll
             for (int jj = 0; jj < B; ++jj) xd[jj] = xv[k][jj];
           }
@@ -581,17 +588,10 @@ __device__ __forceinline__ bool dia_body(int64_t nbr, int nd_rt, const int64_t* 
         const int64_t xb = lower[k] ? ub : (ok[k] ? p + o : p);       // block column
         const double* __restrict__ u = U + dia_at(d, 0, ub, nbr, BB);
         const int64_t qs = dia_q_stride(nbr, BB);
-        if (RCG_DIA_HINT) {
 #pragma unroll
-          for (int jj = 0; jj < B; ++jj) xv[k][jj] = ld_nc_hint(x + B * xb + jj, pol_keep);
+        for (int jj = 0; jj < B; ++jj) xv[k][jj] = __ldg(x + B * xb + jj);
 #pragma unroll
-          for (int q = 0; q < BB; ++q) v[k][q] = ld_nc_hint(u + q * qs, lower[k] ? pol_drop : pol_keep);
-        } else {
-#pragma unroll
-          for (int jj = 0; jj < B; ++jj) xv[k][jj] = __ldg(x + B * xb + jj);
-#pragma unroll
-          for (int q = 0; q < BB; ++q) v[k][q] = __ldg(u + q * qs);
-        }
+        for (int q = 0; q < BB; ++q) v[k][q] = __ldg(u + q * qs);
       }
 #pragma unroll
       for (int k = 0; k < K; ++k) {
@@ -658,182 +658,6 @@ __global__ void __launch_bounds__(kThreads, B == 3 ? RCG_DIA3_MINB : RCG_DIA1_MI
   double d0, d1;
   if (dia_body<B, 1, ND>(sa->n / B, nd, so, sa->dia_values, sa->xs, sa->ys, nullptr, sa->st, d0, d1))
     spmv_epilogue<1>(d0, d1, sa->part, sa->counter, sa->out);
-}
-
-// 3x3 block-DIA with the UPPER blocks staged by TMA (RCG_DIA3_TMA=1).  In the
-// tiled layout the 9 x 32 values of one (diagonal d, 32-block-row tile) are a
-// contiguous 2,304-B run, so lane 0 of each warp streams its tiles' upper runs
-// with cp.async.bulk into a per-warp ring of S stages (mbarrier complete_tx)
-// while the warp computes the lower blocks (U_d(p - o), mostly L2 hits) from
-// registers.  The HBM bytes in flight then sit in shared memory, not in
-// registers.  Per row the FMA order is dia_body's (lower d = nd-1..1, then
-// d = 0..nd-1; jj ascending inside a block), so y is bitwise the same.
-#ifndef RCG_DIA3T_S
-#define RCG_DIA3T_S 4
-#endif
-#ifndef RCG_DIA3T_KU
-#define RCG_DIA3T_KU 7
-#endif
-constexpr int kDiaChunk = 9 * 32;   // doubles per (d, tile) run
-__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void tma_chunk(double* dst, const double* src, uint64_t* bar) {
-  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(kDiaChunk * 8) : "memory");
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   (unsigned)__cvta_generic_to_shared(dst)),
-               "l"(src), "r"(kDiaChunk * 8), "r"(b)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-  unsigned ok = 0;
-  while (!ok) {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(ok)
-        : "r"(b), "r"(parity)
-        : "memory");
-  }
-}
-
-template <int ND>
-__global__ void __launch_bounds__(kThreads, RCG_DIA3_MINB) dia3t_kernel_ind(const SpmvArgs* __restrict__ sa) {
-  // S stages per warp, from the dynamic shared memory size (RCG_DIA3T_S)
-  unsigned dyn;
-  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
-  const int S = (int)(dyn / (kWarps * kDiaChunk * 8));
-  extern __shared__ __align__(128) double ring[];   // [kWarps][S][kDiaChunk]
-  __shared__ __align__(8) uint64_t bars[kWarps][8];
-  __shared__ int64_t so[DIA_MAX];
-  pdl_wait();
-  const int nd = ND > 0 ? ND : sa->dia_nd;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (lane == 0)
-    for (int s = 0; s < S; ++s) mbar_init(&bars[wid][s], 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  dia_load_offsets(nd, sa->dia_offsets, so);   // includes __syncthreads
-  const SolveState* st = sa->st;
-  double d0 = 0.0;
-  if (st->done) return;
-  const long long j = st->j;
-  const double* __restrict__ x = sa->xs.at(j);
-  double* __restrict__ y = sa->ys.at(j);
-  const double* __restrict__ U = sa->dia_values;
-  const int64_t nbr = sa->n / 3, T = (nbr + 31) >> 5;
-  const int64_t tile0 = (int64_t)blockIdx.x * kWarps + wid, tstride = (int64_t)gridDim.x * kWarps;
-  double* myring = ring + (size_t)wid * S * kDiaChunk;
-  // chunk c of this warp's stream: tile tile0 + (c / nd) * tstride, diagonal c % nd
-  auto issue = [&](int64_t c) {
-    const int64_t t = tile0 + (c / nd) * tstride;
-    if (t < T) {
-      const int d = (int)(c % nd);
-      tma_chunk(myring + (c % S) * kDiaChunk, U + ((int64_t)d * T + t) * kDiaChunk, &bars[wid][c % S]);
-    }
-  };
-  if (lane == 0)
-    for (int c = 0; c < S; ++c) issue(c);
-  constexpr int K = RCG_DIA3_K;
-  int64_t c = 0;   // next chunk to consume
-  for (int64_t t = tile0; t < T; t += tstride) {
-    const int64_t pw = t * 32;
-    const bool act = pw + lane < nbr;
-    const int64_t p = act ? pw + lane : nbr - 1;
-    double acc[3] = {0.0, 0.0, 0.0};
-    // lower blocks d = nd-1 .. 1 through registers (as dia_body)
-#pragma unroll(ND > 0 ? (ND - 1 + K - 1) / K : 1)
-    for (int t0 = 0; t0 < nd - 1; t0 += K) {
-      double v[K][9], xv[K][3];
-      bool ok[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int tt = t0 + k;
-        const int d = tt < nd - 1 ? nd - 1 - tt : 1;
-        const int64_t o = so[d];
-        ok[k] = tt < nd - 1 && p >= o;
-        const int64_t ub = ok[k] ? p - o : 0;
-#pragma unroll
-        for (int jj = 0; jj < 3; ++jj) xv[k][jj] = __ldg(x + 3 * ub + jj);
-        const double* __restrict__ u = U + dia_at(d, 0, ub, nbr, 9);
-#pragma unroll
-        for (int q = 0; q < 9; ++q) v[k][q] = __ldg(u + q * 32);
-      }
-#pragma unroll
-      for (int k = 0; k < K; ++k)
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-          for (int jj = 0; jj < 3; ++jj) acc[i] = fma(ok[k] ? v[k][jj * 3 + i] : 0.0, ok[k] ? xv[k][jj] : 0.0, acc[i]);
-    }
-    // diagonal and upper blocks d = 0 .. nd-1 from the TMA ring; the x loads
-    // of KU terms are issued together (L2 latency), then each term waits for
-    // its run, reads it and hands the stage back to the next run
-    constexpr int KU = RCG_DIA3T_KU;
-    double xd[3];
-#pragma unroll(ND > 0 ? (ND + KU - 1) / KU : 1)
-    for (int u0 = 0; u0 < nd; u0 += KU) {
-      double xv[KU][3];
-      bool ok[KU];
-#pragma unroll
-      for (int k = 0; k < KU; ++k) {
-        const int d = u0 + k < nd ? u0 + k : 0;
-        const int64_t o = so[d];
-        ok[k] = u0 + k < nd && p + o < nbr;
-        const int64_t xb = ok[k] ? p + o : p;
-#pragma unroll
-        for (int jj = 0; jj < 3; ++jj) xv[k][jj] = __ldg(x + 3 * xb + jj);
-      }
-      if (u0 == 0) {
-#pragma unroll
-        for (int jj = 0; jj < 3; ++jj) xd[jj] = xv[0][jj];
-      }
-#pragma unroll
-      for (int k = 0; k < KU; ++k) {
-        if (u0 + k >= nd) break;
-        mbar_wait(&bars[wid][c % S], (unsigned)((c / S) & 1));
-        const double* sv = myring + (c % S) * kDiaChunk + lane;
-        double v[9];
-#pragma unroll
-        for (int q = 0; q < 9; ++q) v[q] = sv[q * 32];
-        __syncwarp();
-        if (lane == 0) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue(c + S);
-        }
-        ++c;
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-          for (int jj = 0; jj < 3; ++jj)
-            acc[i] = fma(ok[k] ? v[i * 3 + jj] : 0.0, ok[k] ? xv[k][jj] : 0.0, acc[i]);
-      }
-    }
-    if (!act) continue;
-    const int64_t r = 3 * p;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      d0 += xd[i] * acc[i];
-      y[r + i] = acc[i];
-    }
-  }
-  spmv_epilogue<1>(d0, 0.0, sa->part, sa->counter, sa->out);
-}
-
-static bool dia3_tma() {
-  static const bool on = [] {
-    const char* e = getenv("RCG_DIA3_TMA");
-    return e && atoi(e) != 0;
-  }();
-  return on;
-}
-static size_t dia3t_smem() {
-  static const int S = [] {
-    const char* e = getenv("RCG_DIA3T_S");
-    return e ? std::min(8, std::max(2, atoi(e))) : RCG_DIA3T_S;
-  }();
-  return sizeof(double) * (size_t)kWarps * S * kDiaChunk;
 }
 
 // Exactly one wave of resident CTAs of the kernel actually launched (its own
@@ -1212,13 +1036,6 @@ static int dia_grid_for(Ctx* c, const rcg_csr* A, int mode, bool ind) {
   const int64_t nbr = A->n / A->dia_block;
   const int nd = A->dia_count;
   const void* k;
-  if (A->dia_block == 3 && ind && dia3_tma() && RCG_DIA_TILED) {
-    k = nd == 14 ? (const void*)dia3t_kernel_ind<14> : (const void*)dia3t_kernel_ind<0>;
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, dia3t_smem()) != cudaSuccess || occ < 1)
-      occ = 1;
-    return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nbr, kThreads), (int64_t)c->num_sms * occ));
-  }
   if (A->dia_block == 3) {
     if (ind) k = nd == 14 ? (const void*)dia_kernel_ind<3, 14> : (const void*)dia_kernel_ind<3, 0>;
     else if (nd == 14) k = mode == 0 ? (const void*)dia_kernel<3, 0, 14> : mode == 1 ? (const void*)dia_kernel<3, 1, 14> : (const void*)dia_kernel<3, 2, 14>;
@@ -1305,15 +1122,8 @@ int launch_spmv_ind(Ctx* c, const rcg_csr* A, const SpmvArgs* dargs) {
   size_t smem = 0;
   if (is_dia(A)) {
     const int nd = A->dia_count;
-    if (A->dia_block == 3 && dia3_tma() && RCG_DIA_TILED) {
-      k = nd == 14 ? dia3t_kernel_ind<14> : dia3t_kernel_ind<0>;
-      smem = dia3t_smem();
-      // the attribute is per device: set it on every call (host-side, cheap)
-      RCG_CUDA(c, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    }
     grid = dia_grid_for(c, A, 1, true);
-    if (k) {
-    } else if (A->dia_block == 3) k = nd == 14 ? dia_kernel_ind<3, 14> : dia_kernel_ind<3, 0>;
+    if (A->dia_block == 3) k = nd == 14 ? dia_kernel_ind<3, 14> : dia_kernel_ind<3, 0>;
     else k = nd == 3 ? dia_kernel_ind<1, 3> : (nd == 4 ? dia_kernel_ind<1, 4> : dia_kernel_ind<1, 0>);
   } else if (is_sell3(A)) {
     grid = sell3_grid(c, A->n / 3);

@@ -141,9 +141,24 @@ def check_sequence(rep, spy, g, eps, sols=None, sol_prefix=None, n=None):
     """Apply the bars above; returns the index of the first n_c divergence
     (len(records) when the histories agree throughout)."""
     got_it, want_it = rep.iterations(), g["iterations"]
+    got_nc, want_nc = rep.n_c_history(), g["n_c_before"]
+    if g.get("aborted"):
+        # The reference run itself ends in NumericalFailure("(r, z) <= 0") (c5r:
+        # reorth off, lognormal E).  Which system trips it is rounding-decided
+        # in the reference algorithm: the CPU oracle on the same matrices with
+        # each row's entries stored in reverse order (a rounding-level change
+        # of the SpMV only) aborts at system 1 instead of 9
+        # (tests/test_oracle_golden.py::test_c5r_abort_index_is_rounding_decided).
+        # So: our run must fail the same way, and every system solved on both
+        # sides must meet the bars.
+        assert rep.aborted, "the reference aborts this sequence; ours completed it"
+        fails = [e for e in rep.events if e[0] == "solve_failed"]
+        assert fails and "(r, z) <= 0" in str(fails[-1][-1]), rep.events
+        m = min(len(got_it), len(want_it))
+        assert m >= 1, (got_it, want_it)
+        got_it, want_it, got_nc, want_nc = got_it[:m], want_it[:m], got_nc[:m], want_nc[:m]
     assert len(got_it) == len(want_it), (got_it, want_it)
     assert all(r.converged for r in rep.records) == all(g["converged"])
-    got_nc, want_nc = rep.n_c_history(), g["n_c_before"]
     split = len(got_nc)
     for k in range(len(got_nc)):
         if got_nc[k] != want_nc[k]:

@@ -134,3 +134,34 @@ def test_oracle_pilot_fixture_trks_tol1e6_prefix():
     systems = list(problems.generate_diffusion_sequence(problems.benchmark_spec(seed=0), 10))
     res = orc.run_sequence(systems, strategy="trks", tol=1e-6, max_iters=3000)
     assert res.iterations == g["iterations"][:10]
+
+
+def test_c5r_abort_index_is_rounding_decided():
+    """The reduced config-5 analog (lognormal-E softening elasticity 16^3,
+    reorth off) ends in NumericalFailure("(r, z) <= 0") in the reference run
+    (golden c5r: at system 9).  Which system trips it depends on rounding
+    alone: the same reference algorithm (this oracle) on the same matrices,
+    with each CSR row's entries stored in reverse order - scipy's csr_matvec
+    sums in stored order, so only the SpMV's rounding changes - aborts at an
+    earlier system.  The GPU parity test therefore pins the failure mode and
+    the systems solved on both sides, not the abort index."""
+    g = json.loads((GOLDEN / "reduced_sequences.json").read_text())["c5r"]
+    assert g["aborted"] and g["events"][-1][0] == "solve_failed" and int(g["events"][-1][1]) == 9
+    systems, st = problems.config_systems(5, reduced=True)
+
+    class Rev:
+        def __init__(self, A):
+            ro = np.asarray(A.row_offsets)
+            # reverse every row: entry k of row i moves to ro[i] + ro[i+1] - 1 - k
+            rows = np.repeat(np.arange(A.n), np.diff(ro))
+            src = ro[rows] + ro[rows + 1] - 1 - np.arange(len(rows))
+            self.n, self.nnz, self.row_offsets = A.n, A.nnz, ro
+            self.col_indices = np.asarray(A.col_indices)[src]
+            self.values = np.asarray(A.values)[src]
+
+    rep = orc.run_sequence(((Rev(A), b) for A, b in systems), "srks", epsilon=st["epsilon"],
+                           nc_limit=st["nc_limit"], tol=st["tol"], max_iters=5000, reorthogonalize=False)
+    assert rep.aborted
+    kind, k, msg = rep.events[-1]
+    assert kind == "solve_failed" and "(r, z) <= 0" in msg
+    assert k < 9, (k, rep.iterations)
