@@ -82,7 +82,7 @@ struct IterArgs {
   double* part_z;          // nb
   double* part_reo;        // nb x reo_stride
   int64_t reo_stride;
-  unsigned int* counters;  // [0] spmv [1] update [2] precond [3..] misc
+  unsigned int* counters;  // [0] spmv [1] update [2] precond [3..] misc ([5], [6]: 3x3 DIA tile claims)
   SolveState* st;
   int reorth;
   int rows_per_block;      // K3 row tile
@@ -1698,6 +1698,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     a.spmv.st = st;
     a.spmv.part = part_spmv;
     a.spmv.counter = counters + 0;
+    a.spmv.claim = counters + 5;   // [5] tile claims, [6] mode-0 arrivals (3x3 block-DIA)
     a.spmv.out = gSum.ptr;
     // device copy read by every iteration kernel (pageable source: staged
     // before return, so the host struct may change right after)
@@ -1734,7 +1735,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     if ((rc = allreduce_h(H, c, gSum.ptr + 2, (size_t)n_c))) return fail(rc);
     if ((rc = coarse_combine(c, D, gSum.ptr + 2, nullptr, xext))) return fail(rc);
     if ((rc = halo_exchange(c, H, colsel(xext), nullptr, xext))) return fail(rc);
-    if ((rc = launch_spmv(c, A, 2, colsel(xext), colsel(r), b, nullptr, part_spmv, counters + 0, norms2)))
+    if ((rc = launch_spmv(c, A, 2, colsel(xext), colsel(r), b, nullptr, part_spmv, counters + 0, norms2, counters + 5)))
       return fail(rc);
     RCG_CUDA_F(cudaMemcpyAsync(x, xext, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
   } else {

@@ -490,17 +490,35 @@ __host__ __device__ constexpr int dia_term_diag(int t) {
   return t < ND - 1 ? ND - 1 - t : t - (ND - 1);
 }
 
+#ifndef RCG_DIA3_CLAIM
+#define RCG_DIA3_CLAIM 1   // 3x3: tiles claimed in row order from a device counter
+#endif
+// where the dot-product partials go; read from the argument block only when
+// needed (held in registers across the stream loop they spill its load batch)
+struct DiaOut {
+  const SpmvArgs* sa;
+  double* part_;
+  unsigned int* counter_;
+  unsigned int* claim_;
+  double* out_;
+  __device__ __forceinline__ double* part() const { return sa ? sa->part : part_; }
+  __device__ __forceinline__ unsigned int* counter() const { return sa ? sa->counter : counter_; }
+  __device__ __forceinline__ unsigned int* claim() const { return sa ? sa->claim : claim_; }
+  __device__ __forceinline__ double* out() const { return sa ? sa->out : out_; }
+};
+
 // ND > 0: the diagonal count is a compile-time constant (5/7-point: 3/4
 // upper diagonals, Q1 27-point blocks: 14), so both diagonal loops unroll
 // fully and every value / x load of a row is independent and in flight at
 // once; ND = 0 is the generic runtime-count loop.
 template <int B, int MODE, int ND>
-__device__ __forceinline__ bool dia_body(int64_t nbr, int nd_rt, const int64_t* __restrict__ offs /* smem */,
-                                         const double* __restrict__ U, const ColSel& xs, const ColSel& ys,
-                                         const double* __restrict__ b, const SolveState* st, double& d0, double& d1) {
+__device__ __forceinline__ int dia_body(int64_t nbr, int nd_rt, const int64_t* __restrict__ offs /* smem */,
+                                        const double* __restrict__ U, const ColSel& xs, const ColSel& ys,
+                                        const double* __restrict__ b, const SolveState* st, const DiaOut& o,
+                                        double& d0, double& d1) {
   long long j = 0;
   if (st) {
-    if (st->done) return false;
+    if (st->done) return 0;
     j = st->j;
   }
   const double* __restrict__ x = xs.at(j);
@@ -516,8 +534,8 @@ __device__ __forceinline__ bool dia_body(int64_t nbr, int nd_rt, const int64_t* 
   // (b = 3 only: 833 vs 869 us at 160^3; the scalar stencil prefers the
   // plain per-thread sweep, 162 vs 172 us at 256^3)
   const int lane = B == 3 ? (int)(threadIdx.x & 31) : 0;
-  for (int64_t pw = (int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; pw < nbr;
-       pw += (int64_t)gridDim.x * blockDim.x) {
+  // one block row per thread, starting at block row pw (b = 3: the warp's 32-row tile)
+  auto rows = [&](const int64_t pw) {
     const bool act = pw + lane < nbr;
     const int64_t p = act ? pw + lane : nbr - 1;
     double acc[B];
@@ -609,7 +627,7 @@ __device__ __forceinline__ bool dia_body(int64_t nbr, int nd_rt, const int64_t* 
       }
     }
     }
-    if (!act) continue;
+    if (!act) return;
     const int64_t r = B * p;
     double bv[B];
     if (MODE == 2) {
@@ -630,8 +648,86 @@ __device__ __forceinline__ bool dia_body(int64_t nbr, int nd_rt, const int64_t* 
     }
 #pragma unroll
     for (int i = 0; i < B; ++i) y[r + i] = acc[i];   // no load of this row after its stores
+  };
+  if (B == 3 && RCG_DIA3_CLAIM && o.claim() != nullptr) {
+    // Tiles of 256 block rows are claimed in row order from a device counter
+    // instead of a static grid-stride assignment: rows q and q + o (the two
+    // uses of a far block) are then always o / 256 claims apart in time,
+    // whatever the plane size and however far CTAs have drifted, and there is
+    // no sweep boundary (static: at 160^3 a plane is a third of the grid's
+    // front, DRAM reads 5.7 GB for 4.4 GB of distinct bytes).  Dot partials
+    // are kept per claimed tile and reduced in tile order by the last block,
+    // so the result does not depend on which CTA ran which tile.
+    __shared__ long long s_chunk;
+    __shared__ double s_w[2][kWarps];
+    const int64_t nch = ceil_div(nbr, (int64_t)kThreads);
+    const int wid = threadIdx.x >> 5;
+    constexpr int KP = MODE == 2 ? 2 : 1;
+    if (threadIdx.x == 0) s_chunk = (long long)atomicAdd(o.claim(), 1u);
+    __syncthreads();
+    for (;;) {
+      const int64_t ch = s_chunk;
+      if (ch >= nch) break;
+      d0 = 0.0;
+      d1 = 0.0;
+      rows(ch * kThreads + 32 * wid);
+      if (MODE != 0) {
+        const double t0 = warp_sum(d0);
+        const double t1 = MODE == 2 ? warp_sum(d1) : 0.0;
+        if (lane == 0) {
+          s_w[0][wid] = t0;
+          if (MODE == 2) s_w[1][wid] = t1;
+        }
+      }
+      __syncthreads();   // s_chunk read by all, s_w complete
+      if (threadIdx.x == 0) {
+        if (MODE != 0) {
+          double* part = o.part();
+#pragma unroll
+          for (int k = 0; k < KP; ++k) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) t += s_w[k][w];
+            part[ch * KP + k] = t;
+          }
+        }
+        s_chunk = (long long)atomicAdd(o.claim(), 1u);
+      }
+      __syncthreads();
+    }
+    return 2;
   }
-  return true;
+  for (int64_t pw = (int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; pw < nbr;
+       pw += (int64_t)gridDim.x * blockDim.x)
+    rows(pw);
+  return 1;
+}
+
+// epilogue of the claimed-tile sweep: the last block to arrive sums the per-tile
+// partials in tile order (all threads, fixed tree) and re-arms the claim counter
+template <int MODE>
+__device__ __forceinline__ void dia_claim_epilogue(int64_t nch, const DiaOut& o) {
+  unsigned int* counter = MODE == 0 ? o.claim() + 1 : o.counter();
+  if (!arrive_last(counter)) return;
+  if (threadIdx.x == 0) *o.claim() = 0u;
+  if (MODE == 0) return;
+  __shared__ double sm[kWarps];
+  constexpr int KP = MODE == 2 ? 2 : 1;
+  const double* part = o.part();
+  for (int k = 0; k < KP; ++k) {
+    double s = 0.0;
+    int64_t c = threadIdx.x;
+    for (; c + 7 * kThreads < nch; c += 8 * kThreads) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(part + (c + u * kThreads) * KP + k);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; c < nch; c += kThreads) s += __ldcg(part + c * KP + k);
+    s = block_sum<kThreads>(s, sm);
+    if (threadIdx.x == 0) o.out()[k] = s;
+  }
 }
 
 __device__ __forceinline__ void dia_load_offsets(int nd, const int64_t* __restrict__ g, int64_t* sm) {
@@ -642,11 +738,15 @@ __device__ __forceinline__ void dia_load_offsets(int nd, const int64_t* __restri
 template <int B, int MODE, int ND>
 __global__ void __launch_bounds__(kThreads, B == 3 ? RCG_DIA3_MINB : RCG_DIA1_MINB)
 dia_kernel(int64_t nbr, int nd, const int64_t* __restrict__ offs, const double* __restrict__ U, ColSel xs, ColSel ys,
-           const double* __restrict__ b, const SolveState* st, double* part, unsigned int* counter, double* out) {
+           const double* __restrict__ b, const SolveState* st, double* part, unsigned int* counter,
+           unsigned int* claim, double* out) {
   __shared__ int64_t so[DIA_MAX];
   dia_load_offsets(nd, offs, so);
   double d0, d1;
-  if (dia_body<B, MODE, ND>(nbr, nd, so, U, xs, ys, b, st, d0, d1)) spmv_epilogue<MODE>(d0, d1, part, counter, out);
+  const DiaOut o{nullptr, part, counter, claim, out};
+  const int how = dia_body<B, MODE, ND>(nbr, nd, so, U, xs, ys, b, st, o, d0, d1);
+  if (how == 1) spmv_epilogue<MODE>(d0, d1, part, counter, out);
+  else if (how == 2) dia_claim_epilogue<MODE>(ceil_div(nbr, (int64_t)kThreads), o);
 }
 
 template <int B, int ND>
@@ -656,8 +756,10 @@ __global__ void __launch_bounds__(kThreads, B == 3 ? RCG_DIA3_MINB : RCG_DIA1_MI
   const int nd = sa->dia_nd;
   dia_load_offsets(nd, sa->dia_offsets, so);
   double d0, d1;
-  if (dia_body<B, 1, ND>(sa->n / B, nd, so, sa->dia_values, sa->xs, sa->ys, nullptr, sa->st, d0, d1))
-    spmv_epilogue<1>(d0, d1, sa->part, sa->counter, sa->out);
+  const DiaOut o{sa, nullptr, nullptr, nullptr, nullptr};
+  const int how = dia_body<B, 1, ND>(sa->n / B, nd, so, sa->dia_values, sa->xs, sa->ys, nullptr, sa->st, o, d0, d1);
+  if (how == 1) spmv_epilogue<1>(d0, d1, sa->part, sa->counter, sa->out);
+  else if (how == 2) dia_claim_epilogue<1>(ceil_div(sa->n / B, (int64_t)kThreads), o);
 }
 
 // Exactly one wave of resident CTAs of the kernel actually launched (its own
@@ -1024,11 +1126,12 @@ static inline bool is_sell3(const rcg_csr* A) {
 
 template <int B, int ND>
 static void launch_dia_nd(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const double* b,
-                          const SolveState* st, double* part, unsigned int* counter, double* out) {
+                          const SolveState* st, double* part, unsigned int* counter, double* out,
+                          unsigned int* claim) {
   const int64_t nbr = A->n / B;
   auto k = mode == 0 ? dia_kernel<B, 0, ND> : (mode == 1 ? dia_kernel<B, 1, ND> : dia_kernel<B, 2, ND>);
   k<<<dia_grid(c, nbr, (const void*)k), kThreads, 0, c->stream>>>(nbr, A->dia_count, A->dia_offsets, A->dia_values,
-                                                                  xs, ys, b, st, part, counter, out);
+                                                                  xs, ys, b, st, part, counter, claim, out);
 }
 
 // grid (= partial-sum slots) of the DIA kernel that launch_spmv{,_ind} would use
@@ -1051,22 +1154,23 @@ static int dia_grid_for(Ctx* c, const rcg_csr* A, int mode, bool ind) {
 
 // compile-time diagonal counts: 5-point (3), 7-point (4), Q1 27-point blocks (14)
 static void launch_dia(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const double* b,
-                       const SolveState* st, double* part, unsigned int* counter, double* out) {
+                       const SolveState* st, double* part, unsigned int* counter, double* out,
+                       unsigned int* claim) {
   const int nd = A->dia_count;
   if (A->dia_block == 3) {
-    if (nd == 14) launch_dia_nd<3, 14>(c, A, mode, xs, ys, b, st, part, counter, out);
-    else launch_dia_nd<3, 0>(c, A, mode, xs, ys, b, st, part, counter, out);
+    if (nd == 14) launch_dia_nd<3, 14>(c, A, mode, xs, ys, b, st, part, counter, out, claim);
+    else launch_dia_nd<3, 0>(c, A, mode, xs, ys, b, st, part, counter, out, claim);
   } else {
-    if (nd == 3) launch_dia_nd<1, 3>(c, A, mode, xs, ys, b, st, part, counter, out);
-    else if (nd == 4) launch_dia_nd<1, 4>(c, A, mode, xs, ys, b, st, part, counter, out);
-    else launch_dia_nd<1, 0>(c, A, mode, xs, ys, b, st, part, counter, out);
+    if (nd == 3) launch_dia_nd<1, 3>(c, A, mode, xs, ys, b, st, part, counter, out, claim);
+    else if (nd == 4) launch_dia_nd<1, 4>(c, A, mode, xs, ys, b, st, part, counter, out, claim);
+    else launch_dia_nd<1, 0>(c, A, mode, xs, ys, b, st, part, counter, out, claim);
   }
 }
 
 int launch_spmv(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const double* b,
-                const SolveState* st, double* part, unsigned int* counter, double* out) {
+                const SolveState* st, double* part, unsigned int* counter, double* out, unsigned int* claim) {
   if (is_dia(A)) {
-    launch_dia(c, A, mode, xs, ys, b, st, part, counter, out);
+    launch_dia(c, A, mode, xs, ys, b, st, part, counter, out, claim);
     RCG_LAUNCH_CHECK(c);
     return RCG_OK;
   }
@@ -1164,6 +1268,8 @@ int spmv_partials(Ctx* c, const rcg_csr* A) {
   if (is_dia(A)) {   // partial slots: the widest grid of the modes the solve launches
     int g = dia_grid_for(c, A, 1, true);
     for (int m = 0; m < 3; ++m) g = std::max(g, dia_grid_for(c, A, m, false));
+    // 3x3 with claimed tiles: one slot per 256-block-row tile
+    if (A->dia_block == 3) g = std::max<int64_t>(g, ceil_div(A->n / 3, (int64_t)kThreads));
     return g;
   }
   if (is_sell3(A)) return sell3_grid(c, A->n / 3);
@@ -1230,7 +1336,7 @@ extern "C" int rcg_spmv(rcg_ctx* ctx, const rcg_csr* A, const double* x, double*
     if (rc) return rc;
     if (same && ind == 2) {   // direct mode-1 launch with the same partial buffers
       return launch_spmv(ctx, A, 1, colsel((double*)x), colsel(y), nullptr, nullptr, (double*)(sc + 4096),
-                         (unsigned int*)(sc + 2048), (double*)(sc + 3072));
+                         (unsigned int*)(sc + 2048), (double*)(sc + 3072), (unsigned int*)(sc + 2048 + 64));
     }
     if (same) return launch_spmv_ind(ctx, A, (const SpmvArgs*)sc);
     last[0] = A->values;
@@ -1243,6 +1349,7 @@ extern "C" int rcg_spmv(rcg_ctx* ctx, const rcg_csr* A, const double* x, double*
     h.ys = colsel(y);
     h.st = (const SolveState*)(sc + 1024);
     h.counter = (unsigned int*)(sc + 2048);
+    h.claim = (unsigned int*)(sc + 2048 + 64);
     h.out = (double*)(sc + 3072);
     h.part = (double*)(sc + 4096);
     RCG_CUDA(ctx, cudaMemsetAsync(sc, 0, 4096, ctx->stream));

@@ -19,12 +19,14 @@ struct SpmvArgs {
   double* part;
   unsigned int* counter;
   double* out;
+  unsigned int* claim;   // 3x3 block-DIA: tile claim counter (zero between launches; claim[1]: mode-0 arrivals)
 };
 int launch_spmv_ind(Ctx* c, const rcg_csr* A, const SpmvArgs* dargs);
 void spmv_args_fill(const rcg_csr* A, SpmvArgs* s);
 // mode 0: y = A x; 1: y = A x + (x,y) -> out[0]; 2: y = b - A x + (y,y),(b,b) -> out[0..1]
 int launch_spmv(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const double* b,
-                const SolveState* st, double* part, unsigned int* counter, double* out);
+                const SolveState* st, double* part, unsigned int* counter, double* out,
+                unsigned int* claim = nullptr);
 int spmv_partials(Ctx* c, const rcg_csr* A);
 int spmv_width(const rcg_csr* A);  // number of partial slots per value
 int elementwise_grid(Ctx* c, int64_t n);
