@@ -277,6 +277,27 @@ def test_small_operators_keep_csr_in_production(monkeypatch):
     assert h.dia_count == 0 and h.block == 0
 
 
+def test_dia3_claimed_tiles_bitwise_reproducible(rng):
+    """3x3 block-DIA solve-loop SpMV: 256-row tiles are claimed from a device
+    counter, so which CTA runs which tile differs from launch to launch; the
+    (w, Aw) partials are kept per tile and reduced in tile order, so alpha -
+    and with it the whole trace and x - must not depend on the assignment.
+    n = 70,644 (276 tiles, kernel-sequence loop), two solves, equal bits."""
+    ne = 28
+    A0 = problems.elasticity_q1(ne, E=np.exp(rng.standard_normal((ne,) * 3)))
+    A = rcg.SparseSpdMatrix(A0.n, A0.row_offsets, A0.col_indices, A0.values, validate=False)
+    h = A.device_csr().struct
+    assert h.dia_count == 14 and h.dia_block == 3 and A.n > 49152
+    b = rng.standard_normal(A.n)
+    cfg = rcg.SolveConfig(tol=1e-8, max_iters=120)
+    outs = []
+    for _ in range(3):
+        x, tr = rcg.apcg_solve(A, rcg.Preconditioner.jacobi(A), rcg.build_deflation(A, np.zeros((A.n, 0))), b, cfg)
+        outs.append((np.asarray(x).copy(), np.asarray(tr.alphas).copy(), np.asarray(tr.residual_norms).copy()))
+    for x, al, rn in outs[1:]:
+        assert np.array_equal(x, outs[0][0]) and np.array_equal(al, outs[0][1]) and np.array_equal(rn, outs[0][2])
+
+
 @pytest.mark.parametrize("count,dtype", [(5_000_003, np.float64), (9_000_001, np.int32), (33_554_432 // 8, np.float64)])
 def test_pinned_staged_upload_is_exact(count, dtype):
     """core.h2d (pinned-ring upload used for large CSR arrays) is a plain copy."""

@@ -1,3 +1,3 @@
 #!/bin/bash
-# short, deterministic workload for ncu: 2 systems of config 2, no warmup
-python bench.py --systems 2 --steps 1 --warmup 0 --no-e2e --no-cpu
+# short, deterministic workload for ncu: system 0 of config 3 (the bench's workload), no warmup
+python bench.py --systems 1 --steps 1 --warmup 0 --no-e2e --no-cpu --no-secondary

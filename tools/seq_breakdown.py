@@ -1,4 +1,5 @@
-"""Per-system wall/device time split of the config-2 sequence (diagnostic)."""
+"""Per-system wall/device time split of a sequence (diagnostic).
+usage: python tools/seq_breakdown.py [nelem=64] [count=6] [kind=fixed|softening] [nc_limit=61]"""
 import sys, time
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -8,15 +9,19 @@ from paper_1301_7530_b200 import problems
 
 nelem = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 count = int(sys.argv[2]) if len(sys.argv) > 2 else 6
-seq = list(problems.elasticity_sequence(nelem, count, kind="fixed"))
-A = seq[0][0]
+kind = sys.argv[3] if len(sys.argv) > 3 else "fixed"
+ncl = int(sys.argv[4]) if len(sys.argv) > 4 else 61
+seq = list(problems.elasticity_sequence(nelem, count, kind=kind, device=True))
+for A, _ in seq:
+    A.device_csr()
 bs = [torch.from_numpy(b).cuda() for _, b in seq]
 cfg = rcg.SolveConfig(tol=1e-8, max_iters=20000)
-strat = rcg.RecycleStrategy("srks", epsilon=1e-10, nc_limit=61)
+strat = rcg.RecycleStrategy("srks", epsilon=1e-10, nc_limit=ncl)
 for rep_i in range(2):
     torch.cuda.synchronize(); t0 = time.perf_counter()
-    state = rcg.AugmentationState.from_initial(A.n)
+    state = rcg.AugmentationState.from_initial(seq[0][0].n)
     for k, b in enumerate(bs):
+        A = seq[k][0]
         t1 = time.perf_counter()
         D = rcg.guarded_deflation(A, state, [])
         M = rcg.Preconditioner.jacobi(A)
@@ -28,7 +33,7 @@ for rep_i in range(2):
         torch.cuda.synchronize(); t4 = time.perf_counter()
         rcg.update_basis_srks(state, spec, k)
         torch.cuda.synchronize(); t5 = time.perf_counter()
-        if state.n_c >= 61:
+        if state.n_c >= ncl:
             state.restart()
         m, nsel = spec.m, int(spec.converged_mask.sum())
         del tr, x, spec
