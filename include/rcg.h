@@ -51,7 +51,8 @@ typedef struct rcg_trace rcg_trace;
  * row_offsets is int32 when row_offsets_64 == 0, else int64; col_indices int32.
  * Optional SpMV stream copies (the CSR arrays stay valid and are used by the
  * setup kernels): dia_count > 0 selects the symmetric block-DIA copy (grid
- * operators); else block == 3 selects the 3x3 block copy in bsr_* (built by
+ * operators; on a row slab together with the rem_* ghost-column remainder);
+ * else block == 3 selects the 3x3 block copy in bsr_* (built by
  * rcg_csr_block3_build, optionally sliced): one column index per 9 values,
  * ~29% fewer bytes for vector-valued FEM operators (BASELINE configs 2/3/5). */
 typedef struct {
@@ -72,7 +73,8 @@ typedef struct {
                                        bsr_values [288*slots] */
   int32_t dia_count;                /* > 0: symmetric block-diagonal (DIA) copy */
   int32_t dia_block;                /* DIA unit: 1 (scalar) or 3 (3x3 blocks)  */
-  int32_t pad1;
+  int32_t rem_rows;                 /* row slabs with a DIA copy: number of rows that
+                                       have ghost-column entries (0 = none)     */
   const int64_t* dia_offsets;       /* [dia_count] upper block-diagonal offsets,
                                        ascending, dia_offsets[0] = 0 (device) */
   const double* dia_values;         /* dia_count * b*b * 32*ceil(n/b/32)
@@ -81,6 +83,14 @@ typedef struct {
                                        ((d*T + p/32)*9 + q)*32 + p%32,
                                        T = ceil(n/96); b = 1: A(p, p + off_d)
                                        at d*n + p; 0 = absent */
+  /* Row slabs (sharded operators, columns >= n are ghost entries): the DIA copy
+   * covers the local-local block (a principal submatrix of a symmetric DIA
+   * operator is one too); the ghost-column entries are kept as a compressed
+   * row list and added by a second, small kernel (spmv.cu rem_body). */
+  const int32_t* rem_row_ids;       /* [rem_rows] local row of each listed row    */
+  const int32_t* rem_row_offsets;   /* [rem_rows + 1]                             */
+  const int32_t* rem_col_indices;   /* extended column index (>= n)               */
+  const double* rem_values;
 } rcg_csr;
 
 /* Deflation operator P = I - C G^{-1} (AC)^T, G = C^T A C (DeflationOperator,

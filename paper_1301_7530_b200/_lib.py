@@ -30,8 +30,10 @@ class RcgCsr(C.Structure):
                 ("row_offsets_64", C.c_int32), ("block", C.c_int32),
                 ("col_indices", C.c_void_p), ("values", C.c_void_p),
                 ("bsr_row_offsets", C.c_void_p), ("bsr_col_indices", C.c_void_p), ("bsr_values", C.c_void_p),
-                ("bsr_slice", C.c_int32), ("dia_count", C.c_int32), ("dia_block", C.c_int32), ("pad1", C.c_int32),
-                ("dia_offsets", C.c_void_p), ("dia_values", C.c_void_p)]
+                ("bsr_slice", C.c_int32), ("dia_count", C.c_int32), ("dia_block", C.c_int32), ("rem_rows", C.c_int32),
+                ("dia_offsets", C.c_void_p), ("dia_values", C.c_void_p),
+                ("rem_row_ids", C.c_void_p), ("rem_row_offsets", C.c_void_p), ("rem_col_indices", C.c_void_p),
+                ("rem_values", C.c_void_p)]
 
 
 class RcgDeflation(C.Structure):

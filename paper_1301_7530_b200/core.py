@@ -142,14 +142,38 @@ def colmajor_from_host(M, ld=None):
 
 
 class _DevCsr:
-    __slots__ = ("ro", "ci", "va", "bro", "bci", "bval", "doffs", "dvals", "struct")
+    __slots__ = ("ro", "ci", "va", "bro", "bci", "bval", "doffs", "dvals", "rem", "struct")
 
     def __init__(self, ro, ci, va, n, nnz, ro64):
         self.ro, self.ci, self.va = ro, ci, va
         self.bro = self.bci = self.bval = None
         self.doffs = self.dvals = None
+        self.rem = None
         self.struct = _lib.RcgCsr(n, nnz, ro.data_ptr(), 1 if ro64 else 0, 0, ci.data_ptr(), va.data_ptr(),
                                   None, None, None)
+
+    def add_remainder(self, n, row_offsets, col_indices, values):
+        """Row slab: list the ghost-column entries (local column >= n) as a
+        compressed-row remainder (``rcg_csr.rem_*``), so that the local-local
+        block can take the symmetric block-DIA copy; the slab SpMV is then the
+        DIA kernel plus ``rem_body`` over these rows (spmv.cu)."""
+        torch = _torch()
+        ro = np.asarray(row_offsets, dtype=np.int64)
+        ci = np.asarray(col_indices)
+        ghost = ci >= n
+        if not ghost.any():
+            return
+        rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ro))[ghost]
+        ids, counts = np.unique(rows, return_counts=True)
+        rro = np.concatenate([[0], np.cumsum(counts)])
+        dev = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to("cuda")
+        self.rem = (dev(ids, np.int32), dev(rro, np.int32), dev(ci[ghost], np.int32),
+                    dev(np.asarray(values)[ghost], np.float64))
+        self.struct.rem_rows = len(ids)
+        self.struct.rem_row_ids = self.rem[0].data_ptr()
+        self.struct.rem_row_offsets = self.rem[1].data_ptr()
+        self.struct.rem_col_indices = self.rem[2].data_ptr()
+        self.struct.rem_values = self.rem[3].data_ptr()
 
     def add_dia(self, ctx, b):
         """Attach a symmetric block-DIA copy (spmv.cu ``dia_body``) when every
@@ -322,9 +346,13 @@ class SparseSpdMatrix:
             ci = h2d(np.ascontiguousarray(self.col_indices, dtype=np.int32))
             va = h2d(self.values)
             h = _DevCsr(ro, ci, va, self.n, self.nnz, ro64)
+            self._before_stream_copy(h)
             _maybe_block3(h, self.n, self.nnz, self.use_block3)
             self._dev[dev] = h
         return h
+
+    def _before_stream_copy(self, h):
+        """Hook for subclasses (row slabs attach their ghost-column remainder)."""
 
     def release_device(self):
         """Drop the cached device copy (the next use uploads again)."""

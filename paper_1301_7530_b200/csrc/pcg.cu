@@ -1697,6 +1697,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     a.spmv.ys = a.AW;
     a.spmv.st = st;
     a.spmv.part = part_spmv;
+    a.spmv.rem_part = part_spmv + 2 * (size_t)spmv_main_partials(c, A);
     a.spmv.counter = counters + 0;
     a.spmv.claim = counters + 5;   // [5] tile claims, [6] mode-0 arrivals (3x3 block-DIA)
     a.spmv.out = gSum.ptr;

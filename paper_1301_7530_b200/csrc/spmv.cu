@@ -762,6 +762,83 @@ __global__ void __launch_bounds__(kThreads, B == 3 ? RCG_DIA3_MINB : RCG_DIA1_MI
   else if (how == 2) dia_claim_epilogue<1>(ceil_div(sa->n / B, (int64_t)kThreads), o);
 }
 
+// Ghost-column remainder of a row slab whose local-local block has a DIA copy
+// (rcg_csr.rem_*): y_i (+/-)= sum_k A(i, g_k) x(g_k) over the listed rows, 8
+// lanes per row, after the DIA kernel of the same mode.  MODE 1 adds
+// sum_i x_i t_i to out[0]; MODE 2 (y = b - A x) adds sum_i (y_new^2 - y_old^2).
+// Static assignment and fixed-order partials: reproducible.
+struct RemArgs {
+  int32_t rows;
+  const int32_t* ids;
+  const int32_t* ro;
+  const int32_t* ci;
+  const double* va;
+};
+
+template <int MODE>
+__device__ __forceinline__ void rem_body(const RemArgs& m, const ColSel& xs, const ColSel& ys, const SolveState* st,
+                                         double* part, unsigned int* counter, double* out) {
+  long long j = 0;
+  if (st) {
+    if (st->done) return;
+    j = st->j;
+  }
+  const double* __restrict__ x = xs.at(j);
+  double* __restrict__ y = ys.at(j);
+  const int l8 = threadIdx.x & 7;
+  const int64_t slots = ((int64_t)gridDim.x * blockDim.x) >> 3;
+  double d0 = 0.0;
+  for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3; s < (m.rows + slots - 1) / slots * slots;
+       s += slots) {
+    const bool act = s < m.rows;
+    double t = 0.0;
+    if (act)
+      for (int k = m.ro[s] + l8; k < m.ro[s + 1]; k += 8) t = fma(__ldg(m.va + k), x[m.ci[k]], t);
+    t += __shfl_xor_sync(0xffffffffu, t, 4);
+    t += __shfl_xor_sync(0xffffffffu, t, 2);
+    t += __shfl_xor_sync(0xffffffffu, t, 1);
+    if (act && l8 == 0) {
+      const int64_t i = m.ids[s];
+      const double yo = y[i];
+      if (MODE == 2) {
+        const double yn = yo - t;
+        y[i] = yn;
+        d0 += (yn - yo) * (yn + yo);
+      } else {
+        y[i] = yo + t;
+        if (MODE == 1) d0 += x[i] * t;
+      }
+    }
+  }
+  if (MODE == 0) return;
+  __shared__ double sm[kWarps];
+  const double tb = block_sum<kThreads>(d0, sm);
+  if (threadIdx.x == 0) part[blockIdx.x] = tb;
+  if (arrive_last(counter)) {
+    double s = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += kThreads) s += __ldcg(part + b);
+    s = block_sum<kThreads>(s, sm);
+    if (threadIdx.x == 0) out[0] += s;
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) rem_kernel(RemArgs m, ColSel xs, ColSel ys, const SolveState* st,
+                                                       double* part, unsigned int* counter, double* out) {
+  rem_body<MODE>(m, xs, ys, st, part, counter, out);
+}
+
+__global__ void __launch_bounds__(kThreads) rem_kernel_ind(const SpmvArgs* __restrict__ sa) {
+  pdl_wait();
+  const RemArgs m{sa->rem_rows, sa->rem_ids, sa->rem_ro, sa->rem_ci, sa->rem_va};
+  rem_body<1>(m, sa->xs, sa->ys, sa->st, sa->rem_part, sa->claim + 2, sa->out);
+}
+
+static inline bool has_rem(const rcg_csr* A) { return A->rem_rows > 0 && A->rem_values != nullptr; }
+static int rem_grid(Ctx* c, const rcg_csr* A) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div((int64_t)A->rem_rows * 8, kThreads), 2 * c->num_sms));
+}
+
 // Exactly one wave of resident CTAs of the kernel actually launched (its own
 // occupancy: the variants use 32-100 registers): a grid-stride sweep then
 // moves through the rows as one front, so the lower blocks U_d(p - o) and the
@@ -818,16 +895,18 @@ __device__ __forceinline__ int dia_find(const int64_t* so, int nd, int64_t o) {
 // every entry's block offset must be one of the nd candidates
 template <typename RO>
 __global__ void dia_verify_kernel(int64_t n, int B, const RO* __restrict__ ro, const int32_t* __restrict__ ci,
-                                  const int64_t* __restrict__ offs, int nd, int* bad) {
+                                  const int64_t* __restrict__ offs, int nd, int allow_ghost, int* bad) {
   __shared__ int64_t so[DIA_MAX];
   dia_load_offsets(nd, offs, so);
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t pr = r / B;
-    for (int64_t k = ro[r]; k < ro[r + 1]; ++k)
-      if (ci[k] >= n || dia_find(so, nd, (int64_t)ci[k] / B - pr) < 0) {   // ghost columns: not a DIA operator
+    for (int64_t k = ro[r]; k < ro[r + 1]; ++k) {
+      // ghost columns (row slabs): only with a remainder list attached (rcg_csr.rem_*), which carries them
+      if (ci[k] >= n ? !allow_ghost : dia_find(so, nd, (int64_t)ci[k] / B - pr) < 0) {
         atomicExch(bad, 1);
         return;
       }
+    }
   }
 }
 
@@ -845,6 +924,7 @@ __global__ void dia_fill_kernel(int64_t n, int B, const RO* __restrict__ ro, con
     const int64_t pr = r / B, i = r % B;
     for (int64_t k = ro[r]; k < ro[r + 1]; ++k) {
       const int64_t c = ci[k];
+      if (c >= n) continue;       // ghost column: in the remainder list
       if (c < r) ++lo;
       if (c > r) ++up;
       if (c / B < pr) continue;   // strictly lower block: read from the transpose
@@ -1120,6 +1200,7 @@ static void launch_v(int V, int grid, cudaStream_t s, const rcg_csr* A, ColSel x
 static inline bool is_dia(const rcg_csr* A) {
   return A->dia_count > 0 && A->dia_values && (A->dia_block == 1 || A->dia_block == 3);
 }
+int spmv_main_partials(Ctx* c, const rcg_csr* A);
 static inline bool is_sell3(const rcg_csr* A) {
   return A->block == 3 && A->bsr_slice == 32 && A->bsr_row_offsets;
 }
@@ -1172,6 +1253,16 @@ int launch_spmv(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const 
   if (is_dia(A)) {
     launch_dia(c, A, mode, xs, ys, b, st, part, counter, out, claim);
     RCG_LAUNCH_CHECK(c);
+    if (has_rem(A)) {   // row slab: add the ghost-column entries
+      if (mode != 0 && !claim) return set_error(c, RCG_ERR_CONTRACT, "slab SpMV with a dot product needs counters");
+      const RemArgs m{A->rem_rows, A->rem_row_ids, A->rem_row_offsets, A->rem_col_indices, A->rem_values};
+      double* rp = part ? part + 2 * (size_t)spmv_main_partials(c, A) : nullptr;
+      const int g = rem_grid(c, A);
+      if (mode == 0) rem_kernel<0><<<g, kThreads, 0, c->stream>>>(m, xs, ys, st, rp, nullptr, out);
+      else if (mode == 1) rem_kernel<1><<<g, kThreads, 0, c->stream>>>(m, xs, ys, st, rp, claim + 2, out);
+      else rem_kernel<2><<<g, kThreads, 0, c->stream>>>(m, xs, ys, st, rp, claim + 2, out);
+      RCG_LAUNCH_CHECK(c);
+    }
     return RCG_OK;
   }
   if (is_sell3(A)) {
@@ -1247,6 +1338,10 @@ int launch_spmv_ind(Ctx* c, const rcg_csr* A, const SpmvArgs* dargs) {
   }
   RCG_CUDA(c, launch_k(k, dim3(grid), dim3(kThreads), smem, c->stream, dargs));
   c->launches++;
+  if (is_dia(A) && has_rem(A)) {   // row slab: add the ghost-column entries
+    RCG_CUDA(c, launch_k(rem_kernel_ind, dim3(rem_grid(c, A)), dim3(kThreads), 0, c->stream, dargs));
+    c->launches++;
+  }
   return RCG_OK;
 }
 
@@ -1262,16 +1357,27 @@ void spmv_args_fill(const rcg_csr* A, SpmvArgs* s) {
   s->dia_block = A->dia_block;
   s->dia_offsets = A->dia_offsets;
   s->dia_values = A->dia_values;
+  s->rem_rows = A->rem_rows;
+  s->rem_ids = A->rem_row_ids;
+  s->rem_ro = A->rem_row_offsets;
+  s->rem_ci = A->rem_col_indices;
+  s->rem_va = A->rem_values;
 }
 
-int spmv_partials(Ctx* c, const rcg_csr* A) {
-  if (is_dia(A)) {   // partial slots: the widest grid of the modes the solve launches
+// partial slots of the main SpMV kernel (a slab's remainder kernel keeps its own after 2 x these)
+int spmv_main_partials(Ctx* c, const rcg_csr* A) {
+  if (is_dia(A)) {   // the widest grid of the modes the solve launches
     int g = dia_grid_for(c, A, 1, true);
     for (int m = 0; m < 3; ++m) g = std::max(g, dia_grid_for(c, A, m, false));
     // 3x3 with claimed tiles: one slot per 256-block-row tile
     if (A->dia_block == 3) g = std::max<int64_t>(g, ceil_div(A->n / 3, (int64_t)kThreads));
     return g;
   }
+  return spmv_partials(c, A);
+}
+
+int spmv_partials(Ctx* c, const rcg_csr* A) {
+  if (is_dia(A)) return spmv_main_partials(c, A) + (has_rem(A) ? (rem_grid(c, A) + 1) / 2 + 1 : 0);
   if (is_sell3(A)) return sell3_grid(c, A->n / 3);
   if (A->block == 3 && A->bsr_row_offsets) return bsr3_grid(c, A->n / 3);
   return spmv_grid(c, A, spmv_width(A));
@@ -1329,7 +1435,7 @@ extern "C" int rcg_spmv(rcg_ctx* ctx, const rcg_csr* A, const double* x, double*
     static const void* last[4] = {nullptr, nullptr, nullptr, nullptr};
     const int np = spmv_partials(ctx, A);
     char* sc = nullptr;
-    const size_t need = 4096 + sizeof(double) * (np + 8);
+    const size_t need = 4096 + sizeof(double) * (2 * (size_t)np + 8);
     const bool same = last[0] == A->values && last[1] == x && last[2] == y && last[3] == ctx->scratch &&
                       ctx->scratch_bytes >= need;
     int rc = scratch(ctx, need, (void**)&sc);
@@ -1352,6 +1458,7 @@ extern "C" int rcg_spmv(rcg_ctx* ctx, const rcg_csr* A, const double* x, double*
     h.claim = (unsigned int*)(sc + 2048 + 64);
     h.out = (double*)(sc + 3072);
     h.part = (double*)(sc + 4096);
+    h.rem_part = h.part + 2 * (size_t)spmv_main_partials(ctx, A);
     RCG_CUDA(ctx, cudaMemsetAsync(sc, 0, 4096, ctx->stream));
     RCG_CUDA(ctx, cudaMemcpyAsync(sc, &h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
     RCG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -1511,7 +1618,9 @@ extern "C" int rcg_csr_dia_analyze(rcg_ctx* ctx, const rcg_csr* A, int32_t B, in
   std::vector<int64_t> offs;
   // the longest row's offsets and their negations (a symmetric pattern has
   // both; the first longest row of a small grid may sit on its boundary)
+  const int allow_ghost = A->rem_rows > 0 && A->rem_values != nullptr;
   for (int32_t cc : cols) {
+    if (cc >= A->n) continue;   // ghost column of a row slab
     offs.push_back((int64_t)cc / B - row / B);
     offs.push_back(row / B - (int64_t)cc / B);
   }
@@ -1522,10 +1631,10 @@ extern "C" int rcg_csr_dia_analyze(rcg_ctx* ctx, const rcg_csr* A, int32_t B, in
   RCG_CUDA(ctx, cudaMemcpyAsync(doffs, offs.data(), nd * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
   if (A->row_offsets_64)
     dia_verify_kernel<int64_t><<<g, kThreads, 0, ctx->stream>>>(A->n, B, (const int64_t*)A->row_offsets,
-                                                                A->col_indices, doffs, nd, bad);
+                                                                A->col_indices, doffs, nd, allow_ghost, bad);
   else
     dia_verify_kernel<int32_t><<<g, kThreads, 0, ctx->stream>>>(A->n, B, (const int32_t*)A->row_offsets,
-                                                                A->col_indices, doffs, nd, bad);
+                                                                A->col_indices, doffs, nd, allow_ghost, bad);
   RCG_LAUNCH_CHECK(ctx);
   int hbad = 1;
   RCG_CUDA(ctx, cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));

@@ -19,7 +19,14 @@ struct SpmvArgs {
   double* part;
   unsigned int* counter;
   double* out;
-  unsigned int* claim;   // 3x3 block-DIA: tile claim counter (zero between launches; claim[1]: mode-0 arrivals)
+  unsigned int* claim;   // 3x3 block-DIA: tile claim counter (zero between launches; claim[1]: mode-0
+                         // arrivals; claim[2]: arrivals of the ghost-column remainder kernel)
+  int32_t rem_rows;      // row slab with a DIA copy: ghost-column remainder (rcg.h rcg_csr.rem_*)
+  const int32_t* rem_ids;
+  const int32_t* rem_ro;
+  const int32_t* rem_ci;
+  const double* rem_va;
+  double* rem_part;      // its block partials (after the main kernel's slots)
 };
 int launch_spmv_ind(Ctx* c, const rcg_csr* A, const SpmvArgs* dargs);
 void spmv_args_fill(const rcg_csr* A, SpmvArgs* s);
@@ -28,6 +35,7 @@ int launch_spmv(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const 
                 const SolveState* st, double* part, unsigned int* counter, double* out,
                 unsigned int* claim = nullptr);
 int spmv_partials(Ctx* c, const rcg_csr* A);
+int spmv_main_partials(Ctx* c, const rcg_csr* A);
 int spmv_width(const rcg_csr* A);  // number of partial slots per value
 int elementwise_grid(Ctx* c, int64_t n);
 }  // namespace rcg

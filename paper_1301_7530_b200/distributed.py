@@ -153,6 +153,13 @@ class ShardedMatrix(SparseSpdMatrix):
     def n_ext(self):
         return self.plan.n_local + self.plan.n_ghost
 
+    def _before_stream_copy(self, h):
+        # a slab of a grid operator keeps the symmetric block-DIA stream format:
+        # its local-local block is a principal submatrix (still symmetric, same
+        # diagonals); the ghost-column entries go to a remainder list
+        if self.plan.n_ghost > 0 and os.environ.get("RCG_SLAB_DIA", "1") != "0":
+            h.add_remainder(self.n, self.row_offsets, self.col_indices, self.values)
+
     def halo_struct(self):
         """ctypes rcg_halo with device send lists (cached)."""
         h = self._halo_dev
