@@ -85,12 +85,16 @@ typedef struct {
                                        at d*n + p; 0 = absent */
   /* Row slabs (sharded operators, columns >= n are ghost entries): the DIA copy
    * covers the local-local block (a principal submatrix of a symmetric DIA
-   * operator is one too); the ghost-column entries are kept as a compressed
-   * row list and added by a second, small kernel (spmv.cu rem_body). */
+   * operator is one too); the ghost-column entries are kept as an entry-major
+   * (ELL) list over the rows that have any and added by a second, small kernel
+   * (spmv.cu rem_body). */
   const int32_t* rem_row_ids;       /* [rem_rows] local row of each listed row    */
-  const int32_t* rem_row_offsets;   /* [rem_rows + 1]                             */
-  const int32_t* rem_col_indices;   /* extended column index (>= n)               */
-  const double* rem_values;
+  const int32_t* rem_col_indices;   /* [rem_width * rem_rows] extended column
+                                       index of entry e of listed row s at
+                                       e * rem_rows + s (pads: any valid index)  */
+  const double* rem_values;         /* same layout; pads are 0                    */
+  int32_t rem_width;                /* entries per listed row (max over them)     */
+  int32_t pad2;
 } rcg_csr;
 
 /* Deflation operator P = I - C G^{-1} (AC)^T, G = C^T A C (DeflationOperator,

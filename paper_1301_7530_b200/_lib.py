@@ -32,8 +32,8 @@ class RcgCsr(C.Structure):
                 ("bsr_row_offsets", C.c_void_p), ("bsr_col_indices", C.c_void_p), ("bsr_values", C.c_void_p),
                 ("bsr_slice", C.c_int32), ("dia_count", C.c_int32), ("dia_block", C.c_int32), ("rem_rows", C.c_int32),
                 ("dia_offsets", C.c_void_p), ("dia_values", C.c_void_p),
-                ("rem_row_ids", C.c_void_p), ("rem_row_offsets", C.c_void_p), ("rem_col_indices", C.c_void_p),
-                ("rem_values", C.c_void_p)]
+                ("rem_row_ids", C.c_void_p), ("rem_col_indices", C.c_void_p), ("rem_values", C.c_void_p),
+                ("rem_width", C.c_int32), ("pad2", C.c_int32)]
 
 
 class RcgDeflation(C.Structure):

@@ -154,7 +154,7 @@ class _DevCsr:
 
     def add_remainder(self, n, row_offsets, col_indices, values):
         """Row slab: list the ghost-column entries (local column >= n) as a
-        compressed-row remainder (``rcg_csr.rem_*``), so that the local-local
+        entry-major (ELL) remainder (``rcg_csr.rem_*``), so that the local-local
         block can take the symmetric block-DIA copy; the slab SpMV is then the
         DIA kernel plus ``rem_body`` over these rows (spmv.cu)."""
         torch = _torch()
@@ -164,16 +164,22 @@ class _DevCsr:
         if not ghost.any():
             return
         rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ro))[ghost]
-        ids, counts = np.unique(rows, return_counts=True)
-        rro = np.concatenate([[0], np.cumsum(counts)])
+        ids, first, counts = np.unique(rows, return_index=True, return_counts=True)
+        width, nrow = int(counts.max()), len(ids)
+        # entry-major (ELL) over the listed rows: entry e of listed row s at e * nrow + s, CSR order kept
+        slot = np.arange(len(rows)) - np.repeat(first, counts)
+        srow = np.repeat(np.arange(nrow), counts)
+        eci = np.full((width, nrow), int(ci[ghost][0]), dtype=np.int32)
+        eva = np.zeros((width, nrow), dtype=np.float64)
+        eci[slot, srow] = ci[ghost]
+        eva[slot, srow] = np.asarray(values)[ghost]
         dev = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to("cuda")
-        self.rem = (dev(ids, np.int32), dev(rro, np.int32), dev(ci[ghost], np.int32),
-                    dev(np.asarray(values)[ghost], np.float64))
-        self.struct.rem_rows = len(ids)
+        self.rem = (dev(ids, np.int32), dev(eci, np.int32), dev(eva, np.float64))
+        self.struct.rem_rows = nrow
+        self.struct.rem_width = width
         self.struct.rem_row_ids = self.rem[0].data_ptr()
-        self.struct.rem_row_offsets = self.rem[1].data_ptr()
-        self.struct.rem_col_indices = self.rem[2].data_ptr()
-        self.struct.rem_values = self.rem[3].data_ptr()
+        self.struct.rem_col_indices = self.rem[1].data_ptr()
+        self.struct.rem_values = self.rem[2].data_ptr()
 
     def add_dia(self, ctx, b):
         """Attach a symmetric block-DIA copy (spmv.cu ``dia_body``) when every

@@ -763,14 +763,18 @@ __global__ void __launch_bounds__(kThreads, B == 3 ? RCG_DIA3_MINB : RCG_DIA1_MI
 }
 
 // Ghost-column remainder of a row slab whose local-local block has a DIA copy
-// (rcg_csr.rem_*): y_i (+/-)= sum_k A(i, g_k) x(g_k) over the listed rows, 8
-// lanes per row, after the DIA kernel of the same mode.  MODE 1 adds
-// sum_i x_i t_i to out[0]; MODE 2 (y = b - A x) adds sum_i (y_new^2 - y_old^2).
-// Static assignment and fixed-order partials: reproducible.
+// (rcg_csr.rem_*): y_i (+/-)= sum_e A(i, g_e) x(g_e) over the listed rows, after
+// the DIA kernel of the same mode.  The list is entry-major (ELL over the
+// listed rows, padded with zeros): thread per row, every index / value load
+// coalesced and independent, then the x gathers: two memory round trips per
+// 16 entries (a compressed-row version with a warp per row chained four
+// dependent loads per row and took 42 us for 57 k rows; this one: see
+// profiles/r02z_slab_spmv.log).  MODE 1 adds sum_i x_i t_i to out[0]; MODE 2
+// (y = b - A x) adds sum_i (y_new^2 - y_old^2).  Static assignment and
+// fixed-order partials: reproducible.
 struct RemArgs {
-  int32_t rows;
+  int32_t rows, width;
   const int32_t* ids;
-  const int32_t* ro;
   const int32_t* ci;
   const double* va;
 };
@@ -785,29 +789,34 @@ __device__ __forceinline__ void rem_body(const RemArgs& m, const ColSel& xs, con
   }
   const double* __restrict__ x = xs.at(j);
   double* __restrict__ y = ys.at(j);
-  const int l8 = threadIdx.x & 7;
-  const int64_t slots = ((int64_t)gridDim.x * blockDim.x) >> 3;
+  constexpr int CH = 16;
   double d0 = 0.0;
-  for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3; s < (m.rows + slots - 1) / slots * slots;
-       s += slots) {
-    const bool act = s < m.rows;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < m.rows; s += (int64_t)gridDim.x * blockDim.x) {
     double t = 0.0;
-    if (act)
-      for (int k = m.ro[s] + l8; k < m.ro[s + 1]; k += 8) t = fma(__ldg(m.va + k), x[m.ci[k]], t);
-    t += __shfl_xor_sync(0xffffffffu, t, 4);
-    t += __shfl_xor_sync(0xffffffffu, t, 2);
-    t += __shfl_xor_sync(0xffffffffu, t, 1);
-    if (act && l8 == 0) {
-      const int64_t i = m.ids[s];
-      const double yo = y[i];
-      if (MODE == 2) {
-        const double yn = yo - t;
-        y[i] = yn;
-        d0 += (yn - yo) * (yn + yo);
-      } else {
-        y[i] = yo + t;
-        if (MODE == 1) d0 += x[i] * t;
+    for (int e0 = 0; e0 < m.width; e0 += CH) {
+      int c[CH];
+      double v[CH], xv[CH];
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        const bool ok = e0 + u < m.width;
+        const int64_t at = (int64_t)(ok ? e0 + u : 0) * m.rows + s;
+        c[u] = __ldg(m.ci + at);
+        v[u] = ok ? __ldg(m.va + at) : 0.0;
       }
+#pragma unroll
+      for (int u = 0; u < CH; ++u) xv[u] = x[c[u]];
+#pragma unroll
+      for (int u = 0; u < CH; ++u) t = fma(v[u], xv[u], t);
+    }
+    const int64_t i = m.ids[s];
+    const double yo = y[i];
+    if (MODE == 2) {
+      const double yn = yo - t;
+      y[i] = yn;
+      d0 += (yn - yo) * (yn + yo);
+    } else {
+      y[i] = yo + t;
+      if (MODE == 1) d0 += x[i] * t;
     }
   }
   if (MODE == 0) return;
@@ -815,10 +824,10 @@ __device__ __forceinline__ void rem_body(const RemArgs& m, const ColSel& xs, con
   const double tb = block_sum<kThreads>(d0, sm);
   if (threadIdx.x == 0) part[blockIdx.x] = tb;
   if (arrive_last(counter)) {
-    double s = 0.0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += kThreads) s += __ldcg(part + b);
-    s = block_sum<kThreads>(s, sm);
-    if (threadIdx.x == 0) out[0] += s;
+    double sum = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += kThreads) sum += __ldcg(part + b);
+    sum = block_sum<kThreads>(sum, sm);
+    if (threadIdx.x == 0) out[0] += sum;
   }
 }
 
@@ -830,13 +839,13 @@ __global__ void __launch_bounds__(kThreads) rem_kernel(RemArgs m, ColSel xs, Col
 
 __global__ void __launch_bounds__(kThreads) rem_kernel_ind(const SpmvArgs* __restrict__ sa) {
   pdl_wait();
-  const RemArgs m{sa->rem_rows, sa->rem_ids, sa->rem_ro, sa->rem_ci, sa->rem_va};
+  const RemArgs m{sa->rem_rows, sa->rem_width, sa->rem_ids, sa->rem_ci, sa->rem_va};
   rem_body<1>(m, sa->xs, sa->ys, sa->st, sa->rem_part, sa->claim + 2, sa->out);
 }
 
-static inline bool has_rem(const rcg_csr* A) { return A->rem_rows > 0 && A->rem_values != nullptr; }
+static inline bool has_rem(const rcg_csr* A) { return A->rem_rows > 0 && A->rem_width > 0 && A->rem_values != nullptr; }
 static int rem_grid(Ctx* c, const rcg_csr* A) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div((int64_t)A->rem_rows * 8, kThreads), 2 * c->num_sms));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div((int64_t)A->rem_rows, kThreads), 8 * c->num_sms));
 }
 
 // Exactly one wave of resident CTAs of the kernel actually launched (its own
@@ -1255,12 +1264,11 @@ int launch_spmv(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const 
     RCG_LAUNCH_CHECK(c);
     if (has_rem(A)) {   // row slab: add the ghost-column entries
       if (mode != 0 && !claim) return set_error(c, RCG_ERR_CONTRACT, "slab SpMV with a dot product needs counters");
-      const RemArgs m{A->rem_rows, A->rem_row_ids, A->rem_row_offsets, A->rem_col_indices, A->rem_values};
+      const RemArgs m{A->rem_rows, A->rem_width, A->rem_row_ids, A->rem_col_indices, A->rem_values};
       double* rp = part ? part + 2 * (size_t)spmv_main_partials(c, A) : nullptr;
       const int g = rem_grid(c, A);
-      if (mode == 0) rem_kernel<0><<<g, kThreads, 0, c->stream>>>(m, xs, ys, st, rp, nullptr, out);
-      else if (mode == 1) rem_kernel<1><<<g, kThreads, 0, c->stream>>>(m, xs, ys, st, rp, claim + 2, out);
-      else rem_kernel<2><<<g, kThreads, 0, c->stream>>>(m, xs, ys, st, rp, claim + 2, out);
+      auto k = mode == 0 ? rem_kernel<0> : mode == 1 ? rem_kernel<1> : rem_kernel<2>;
+      k<<<g, kThreads, 0, c->stream>>>(m, xs, ys, st, rp, mode == 0 ? nullptr : claim + 2, out);
       RCG_LAUNCH_CHECK(c);
     }
     return RCG_OK;
@@ -1358,8 +1366,8 @@ void spmv_args_fill(const rcg_csr* A, SpmvArgs* s) {
   s->dia_offsets = A->dia_offsets;
   s->dia_values = A->dia_values;
   s->rem_rows = A->rem_rows;
+  s->rem_width = A->rem_width;
   s->rem_ids = A->rem_row_ids;
-  s->rem_ro = A->rem_row_offsets;
   s->rem_ci = A->rem_col_indices;
   s->rem_va = A->rem_values;
 }
@@ -1618,7 +1626,7 @@ extern "C" int rcg_csr_dia_analyze(rcg_ctx* ctx, const rcg_csr* A, int32_t B, in
   std::vector<int64_t> offs;
   // the longest row's offsets and their negations (a symmetric pattern has
   // both; the first longest row of a small grid may sit on its boundary)
-  const int allow_ghost = A->rem_rows > 0 && A->rem_values != nullptr;
+  const int allow_ghost = A->rem_rows > 0 && A->rem_width > 0 && A->rem_values != nullptr;
   for (int32_t cc : cols) {
     if (cc >= A->n) continue;   // ghost column of a row slab
     offs.push_back((int64_t)cc / B - row / B);

@@ -22,8 +22,8 @@ struct SpmvArgs {
   unsigned int* claim;   // 3x3 block-DIA: tile claim counter (zero between launches; claim[1]: mode-0
                          // arrivals; claim[2]: arrivals of the ghost-column remainder kernel)
   int32_t rem_rows;      // row slab with a DIA copy: ghost-column remainder (rcg.h rcg_csr.rem_*)
+  int32_t rem_width;
   const int32_t* rem_ids;
-  const int32_t* rem_ro;
   const int32_t* rem_ci;
   const double* rem_va;
   double* rem_part;      // its block partials (after the main kernel's slots)
