@@ -449,6 +449,8 @@ __host__ __device__ __forceinline__ int64_t dia_q_stride(int64_t nbr, int BB) {
 #endif
 #ifndef RCG_DIA3_MINB
 #define RCG_DIA3_MINB 2   // 128 registers: 2 CTAs/SM with 4 blocks (48 loads) in flight per thread
+                          // (re-swept on the paired-order / claimed-tile body at Q1 96^3: K=4, 2 CTAs 156 us;
+                          //  K=3, 3 CTAs 163 us; K=2, 4 CTAs 183 us)
 #endif
 
 #ifndef RCG_DIA_FAST
