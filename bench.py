@@ -214,8 +214,10 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(args, A.n, A.nnz, 1),
+        "higher_is_better": True, "scaling": "strong" if (world > 1 and not args.replicas) else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        # the same config dict as our arm at this N (the CPU arm itself always runs on rank 0's host cores)
+        "config": config_dict(args, A.n, A.nnz, world, world > 1 and not args.replicas),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": ncpu, "blas_threads": blas_threads(), "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -333,7 +335,12 @@ def run_ours(args):
         D.init_comm()
     systems = device_systems(args, rank, world, sharded)
     n_global = 3 * nelem * (nelem + 1) ** 2
-    nnz_global = int(systems[0][0].nnz) if not sharded else None
+    nnz_global = int(systems[0][0].nnz)
+    if sharded:   # slabs hold whole rows: the global count is the sum over ranks
+        import torch.distributed as dist
+        t = torch.tensor([nnz_global], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t)
+        nnz_global = int(t.item())
 
     def barrier():
         if world > 1:
