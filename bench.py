@@ -71,6 +71,8 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-secondary", action="store_true")
     p.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of row sharding")
+    p.add_argument("--shard-one", action="store_true",
+                   help="diagnostic: run the row-sharded code path with a 1-rank NCCL communicator (under torchrun, N = 1)")
     return p.parse_args()
 
 
@@ -320,7 +322,7 @@ def run_ours(args):
     import torch
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.shard_one:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_1301_7530_b200 as rcg
@@ -329,7 +331,7 @@ def run_ours(args):
     nelem, count, kind, ncl = shape(args)
     cfg = rcg.SolveConfig(tol=1e-8, max_iters=args.max_iters, reorthogonalize=True)
     strat = rcg.RecycleStrategy("srks", epsilon=1e-10, nc_limit=ncl)
-    sharded = world > 1 and not args.replicas
+    sharded = (world > 1 and not args.replicas) or args.shard_one
     if sharded:
         from paper_1301_7530_b200 import distributed as D
         D.init_comm()
@@ -553,11 +555,11 @@ def run_ours(args):
                            for k, v in sorted(per_system.items())},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "secondary": secondary,
             "phases_profiled_step": ({"kernels_seconds": sum(s["seconds"] for s in stats.values()), **phases}
-                                     if world > 1 else None),
+                                     if (world > 1 or args.shard_one) else None),
             "gpu_launches": launches, "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or args.shard_one:
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
