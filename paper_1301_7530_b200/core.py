@@ -141,6 +141,29 @@ def colmajor_from_host(M, ld=None):
 # CSR operator
 
 
+def ghost_remainder_ell(n, row_offsets, col_indices, values):
+    """The entries of a row slab whose (local) column is >= n, i.e. its ghost
+    columns, as an ELL list over the rows that have any: ``(row_ids[int32 R],
+    cols[int32 W x R], vals[float64 W x R])`` with entry e of listed row s at
+    ``[e, s]``, CSR order kept, pads = (a valid column, 0.0).  None when the
+    slab has no ghost entries.  Host-side (numpy); layout of ``rcg_csr.rem_*``."""
+    ro = np.asarray(row_offsets, dtype=np.int64)
+    ci = np.asarray(col_indices)
+    ghost = ci >= n
+    if not ghost.any():
+        return None
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ro))[ghost]
+    ids, first, counts = np.unique(rows, return_index=True, return_counts=True)
+    width, nrow = int(counts.max()), len(ids)
+    slot = np.arange(len(rows)) - np.repeat(first, counts)
+    srow = np.repeat(np.arange(nrow), counts)
+    eci = np.full((width, nrow), int(ci[ghost][0]), dtype=np.int32)
+    eva = np.zeros((width, nrow), dtype=np.float64)
+    eci[slot, srow] = ci[ghost]
+    eva[slot, srow] = np.asarray(values, dtype=np.float64)[ghost]
+    return ids.astype(np.int32), eci, eva
+
+
 class _DevCsr:
     __slots__ = ("ro", "ci", "va", "bro", "bci", "bval", "doffs", "dvals", "rem", "struct")
 
@@ -153,30 +176,19 @@ class _DevCsr:
                                   None, None, None)
 
     def add_remainder(self, n, row_offsets, col_indices, values):
-        """Row slab: list the ghost-column entries (local column >= n) as a
+        """Row slab: list the ghost-column entries (local column >= n) as an
         entry-major (ELL) remainder (``rcg_csr.rem_*``), so that the local-local
         block can take the symmetric block-DIA copy; the slab SpMV is then the
         DIA kernel plus ``rem_body`` over these rows (spmv.cu)."""
         torch = _torch()
-        ro = np.asarray(row_offsets, dtype=np.int64)
-        ci = np.asarray(col_indices)
-        ghost = ci >= n
-        if not ghost.any():
+        ell = ghost_remainder_ell(n, row_offsets, col_indices, values)
+        if ell is None:
             return
-        rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ro))[ghost]
-        ids, first, counts = np.unique(rows, return_index=True, return_counts=True)
-        width, nrow = int(counts.max()), len(ids)
-        # entry-major (ELL) over the listed rows: entry e of listed row s at e * nrow + s, CSR order kept
-        slot = np.arange(len(rows)) - np.repeat(first, counts)
-        srow = np.repeat(np.arange(nrow), counts)
-        eci = np.full((width, nrow), int(ci[ghost][0]), dtype=np.int32)
-        eva = np.zeros((width, nrow), dtype=np.float64)
-        eci[slot, srow] = ci[ghost]
-        eva[slot, srow] = np.asarray(values)[ghost]
-        dev = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to("cuda")
-        self.rem = (dev(ids, np.int32), dev(eci, np.int32), dev(eva, np.float64))
-        self.struct.rem_rows = nrow
-        self.struct.rem_width = width
+        ids, eci, eva = ell
+        dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to("cuda")
+        self.rem = (dev(ids), dev(eci), dev(eva))
+        self.struct.rem_rows = len(ids)
+        self.struct.rem_width = eci.shape[0]
         self.struct.rem_row_ids = self.rem[0].data_ptr()
         self.struct.rem_col_indices = self.rem[1].data_ptr()
         self.struct.rem_values = self.rem[2].data_ptr()

@@ -92,3 +92,35 @@ def test_partition_rows_balanced_and_aligned():
         assert np.all(bd % 3 == 0)
         nnz = np.diff(A.row_offsets[bd])
         assert nnz.max() <= 1.2 * nnz.mean() + 81 * 3
+
+
+@pytest.mark.parametrize("kind", ["elasticity", "diffusion"])
+def test_slab_local_block_plus_ghost_remainder(kind):
+    """The slab SpMV split used on the device (spmv.cu dia kernel + rem_body):
+    rows of a slab = (local-local block) x_local + (ELL ghost-column remainder)
+    x_ghost.  The local-local block of every slab is symmetric (so it can take
+    the symmetric block-DIA copy), the remainder keeps CSR order, pads are
+    zeros, and the two parts reproduce the global product's slab rows."""
+    import scipy.sparse as sp
+    from paper_1301_7530_b200.core import ghost_remainder_ell
+    from paper_1301_7530_b200.distributed import local_systems_all
+    A, _, align = _problem(kind)
+    G = sp.csr_matrix((A.values, A.col_indices, A.row_offsets), shape=(A.n, A.n))
+    x = np.random.default_rng(11).standard_normal(A.n)
+    y = G @ x
+    bounds = partition_rows(A.row_offsets, 3, align=align)
+    for r, (ro, lci, va, plan) in enumerate(local_systems_all(A.row_offsets, A.col_indices, A.values, bounds)):
+        nl = plan.n_local
+        S = sp.csr_matrix((va, lci, ro), shape=(nl, nl + plan.n_ghost))
+        LL = S[:, :nl]
+        assert abs(LL - LL.T).max() == 0.0                      # principal submatrix: still symmetric
+        ids, eci, eva = ghost_remainder_ell(nl, ro, lci, va)
+        assert eci.dtype == np.int32 and eci.shape == eva.shape and eci.min() >= nl
+        assert np.count_nonzero(eva) <= S[:, nl:].nnz and len(ids) == len(np.unique(S[:, nl:].nonzero()[0]))
+        xe = np.concatenate([x[bounds[r]:bounds[r + 1]], x[plan.ghost_global]])
+        t = np.zeros(nl)
+        for e in range(eci.shape[0]):                           # entry by entry, as rem_body
+            t[ids] += eva[e] * xe[eci[e]]
+        got = LL @ xe[:nl] + t
+        want = y[bounds[r]:bounds[r + 1]]
+        np.testing.assert_allclose(got, want, rtol=1e-13, atol=1e-13 * np.abs(want).max())
