@@ -416,7 +416,8 @@ int sell3_grid(Ctx* c, int64_t nbr) {
 // stream (values at p and at p - o, x at b(p +- o)), no column indices are
 // read, and each stored block feeds two rows: 8 b^2 nd bytes per block row
 // instead of 12 bytes per stored entry.  Row sums accumulate entry by entry
-// in ascending column order (the CSR order).
+// in ascending column order (the CSR order); interior rows of the 3x3 variant
+// take the far diagonals first (dia_term_*, below).
 
 constexpr int DIA_MAX = 64;
 
@@ -851,10 +852,11 @@ static int rem_grid(Ctx* c, const rcg_csr* A) {
 }
 
 // Exactly one wave of resident CTAs of the kernel actually launched (its own
-// occupancy: the variants use 32-100 registers): a grid-stride sweep then
-// moves through the rows as one front, so the lower blocks U_d(p - o) and the
-// x entries at p - o are still in L2 when row p reads them (a second wave
-// re-reads them from HBM: +19% bytes and 2x the time at 256^3).
+// occupancy: the variants use 64-128 registers): the sweep (grid-stride for
+// the scalar variant, tiles claimed in row order for 3x3) then moves through
+// the rows as one front, so the lower blocks U_d(p - o) and the x entries at
+// p - o are still in L2 when row p reads them (a second wave re-reads them
+// from HBM: +19% bytes and 2x the time at 256^3).
 int occupancy_of(const void* kernel) {
   static std::mutex mu;
   static std::map<const void*, int> cache;
