@@ -48,6 +48,17 @@ constexpr int kGemvUnroll = RCG_GEMV_UNROLL;
 #ifndef RCG_WU_KB
 #define RCG_WU_KB 2     // K5 columns per explicit load batch (x RPT/2 128-bit loads)
 #endif
+// no-reorth K3 (z pass only): CTAs/SM and rows per thread per step.  At the
+// former 4 CTAs/SM (64 registers) the body spilled 168 B of stack; 2 CTAs/SM
+// with 8 rows (16 loads) in flight per thread has no spills: config 4
+// (7-point 256^3) 4,220 -> 4,690 GB/s; 3 CTAs x 4 rows 3,990, 3 x 8 2,530
+// (spills), 2 x 4 4,090.  Same rows per thread in the same order: same bits.
+#ifndef RCG_PRE_LEAN_MINB
+#define RCG_PRE_LEAN_MINB 2
+#endif
+#ifndef RCG_PRE_ZB_LEAN
+#define RCG_PRE_ZB_LEAN 8
+#endif
 #ifndef RCG_ACTR_PIPE
 #define RCG_ACTR_PIPE 1
 #endif
@@ -506,10 +517,10 @@ coarse_kernel(const IterArgs* __restrict__ ap, int check_done) {
 // ---------------------------------------------------------------------------
 // K3: convergence test, z = M^{-1} r - C s, (r, z), reorth partials
 
-// REO = false: the lean no-reorth variant (no GEMV code, so no 128-register
-// budget): 4 CTAs/SM keep enough row loads in flight for the z pass
+// REO = false: the lean no-reorth variant (no GEMV code): RCG_PRE_LEAN_MINB
+// CTAs/SM with RCG_PRE_ZB_LEAN rows in flight per thread for the z pass
 template <int CG, bool PF, bool REO>
-__global__ void __launch_bounds__(kThreads, REO ? RCG_PRE_MINB : 4)
+__global__ void __launch_bounds__(kThreads, REO ? RCG_PRE_MINB : RCG_PRE_LEAN_MINB)
 precond_kernel(const IterArgs* __restrict__ ap, int init) {
   pdl_wait();
   const IterArgs& a = *ap;
@@ -565,7 +576,7 @@ precond_kernel(const IterArgs* __restrict__ ap, int init) {
   // step's stores (z may alias r / W for the compiler, which would otherwise
   // serialize one HBM round trip per row); rows i, i + 256, ... keep the
   // per-thread (r, z) summation order of a plain row loop
-  constexpr int ZB = 4;
+  constexpr int ZB = RCG_PRE_ZB_LEAN > 0 && !REO ? RCG_PRE_ZB_LEAN : 4;
   for (int64_t ib = r0 + threadIdx.x; ib < r1; ib += ZB * kThreads) {
     double rv[ZB], zv[ZB], wv[ZB];
 #pragma unroll
