@@ -555,9 +555,11 @@ __device__ __forceinline__ int dia_body(int64_t nbr, int nd_rt, const int64_t* _
     double xd[B];   // x of this block row (the o = 0 block), kept for the (x, y) dot
     // Interior rows (every block of the stencil in range: all but the first
     // and last o_max block rows) skip the range predicates, clamps and the
-    // zero selects: same loads, same FMA order and operands, so the same
-    // bits, at about a third of the instructions (ncu r02: the general body
-    // issues 193 instructions per 7-point row, 1,905 per 3x3 block row).
+    // zero selects: same loads and FMA operands (and, for b = 1 or
+    // RCG_DIA3_ORDER=0, the same order, so the same bits; the 3x3 body sums in
+    // the dia_term_* order), at about a third of the instructions (ncu r02:
+    // the general body issues 193 instructions per 7-point row, 1,905 per 3x3
+    // block row).
     if (RCG_DIA_FAST && ND > 0 && pw >= offs[nd - 1] && pw + (B == 3 ? 31 : 0) + offs[nd - 1] < nbr) {
 #pragma unroll
       for (int t0 = 0; t0 < 2 * ND - 1; t0 += K) {
