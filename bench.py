@@ -559,6 +559,9 @@ def run_ours(args):
             "gpu_launches": launches, "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
+    if sharded:
+        from paper_1301_7530_b200 import distributed as D
+        D.destroy_comm()            # graphs, then the communicator: nothing NCCL left for interpreter exit
     if world > 1 or args.shard_one:
         import torch.distributed as dist
         dist.destroy_process_group()

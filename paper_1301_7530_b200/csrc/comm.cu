@@ -207,8 +207,19 @@ __global__ void halo_pack_kernel(int64_t total, const int32_t* __restrict__ idx,
     out[k] = s[idx[k]];
 }
 
+// The exchange runs with peers, or - RCG_COMM_FORCE=1 on a 1-rank NCCL
+// communicator with a plan that lists ghost copies of the rank's own rows
+// (two virtual slabs in one rank, tests/test_gpu_solver.py) - as a send /
+// recv to self, so the whole pack -> ncclSend/ncclRecv -> unpack path and its
+// CUDA-graph capture can be exercised on one GPU.
+static bool halo_active(const Ctx* c, const rcg_halo* H) {
+  if (!H || !c->comm) return false;
+  if (c->comm->nranks > 1) return true;
+  return comm_force() && !c->comm->loop && c->comm->comm && H->n_ghost > 0;
+}
+
 int halo_exchange(Ctx* c, const rcg_halo* H, ColSel src, const SolveState* st, double* dst_col) {
-  if (!H || !c->comm || c->comm->nranks <= 1) return RCG_OK;
+  if (!halo_active(c, H)) return RCG_OK;
   if (c->comm->loop) {
     // loopback: the single send buffer may be repacked only after every rank
     // consumed the previous exchange (events recorded before the last barrier)
@@ -226,8 +237,9 @@ int halo_exchange(Ctx* c, const rcg_halo* H, ColSel src, const SolveState* st, d
   if (c->comm->loop) return loop_halo(c, H, dst_col);
   Nccl& api = c->comm->api;
   RCG_NCCL(c, api.groupStart());
+  const bool self = c->comm->nranks <= 1;   // forced self exchange (halo_active)
   for (int q = 0; q < H->nranks; ++q) {
-    if (q == H->rank) continue;
+    if (q == H->rank && !self) continue;
     const int64_t ns = H->send_off[q + 1] - H->send_off[q];
     const int64_t nr = H->recv_off[q + 1] - H->recv_off[q];
     if (ns > 0) RCG_NCCL(c, api.send(H->send_buf + H->send_off[q], (size_t)ns, kNcclFloat64, q, c->comm->comm, c->stream));
@@ -260,7 +272,7 @@ int halo_prepare(Ctx* c, const rcg_halo* H) {
 }
 
 int halo_exchange_dev(Ctx* c, const rcg_halo* H, ColSel src, const SolveState* st, ColSel dst) {
-  if (!H || !c->comm || c->comm->nranks <= 1) return RCG_OK;
+  if (!halo_active(c, H)) return RCG_OK;
   if (H->n_ghost > (int64_t)c->halo_recv_cap)
     return set_error(c, RCG_ERR_CONTRACT, "halo staging not prepared (halo_prepare before the solve loop)");
   // received ghosts land at halo_recv + recv_off[q] (the exchange's "column"
@@ -276,6 +288,12 @@ int halo_exchange_dev(Ctx* c, const rcg_halo* H, ColSel src, const SolveState* s
 }
 
 void comm_free(Ctx* c) {
+  // captured batches hold this communicator's send / recv / allreduce nodes:
+  // NCCL requires the graphs to go first (ncclCommDestroy otherwise blocks:
+  // seen as a hang at process exit once halo send / recv were captured)
+  cudaStreamSynchronize(c->stream);
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.second.exec);
+  c->graphs.clear();
   if (c->halo_recv) {
     cudaFree(c->halo_recv);
     c->halo_recv = nullptr;

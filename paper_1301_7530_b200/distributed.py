@@ -32,6 +32,7 @@ from . import _lib
 from .core import ContractViolation, SparseSpdMatrix
 
 __all__ = ["partition_rows", "HaloPlan", "build_local_system", "local_systems_all", "ShardedMatrix", "init_comm",
+           "destroy_comm",
            "init_loopback", "LoopbackGroup", "nccl_library"]
 
 
@@ -206,6 +207,14 @@ def init_comm(group=None):
     idb = (C.c_char * 128).from_buffer_copy(obj[0])
     ctx.check(ctx.lib.rcg_comm_init(ctx.h, pb, idb, world, rank), "nccl comm init")
     return ctx
+
+
+def destroy_comm():
+    """Tear down this thread's communicator (captured batch graphs first, then
+    ncclCommDestroy): call before ``torch.distributed.destroy_process_group``
+    / process exit so that no NCCL teardown is left to interpreter shutdown."""
+    ctx = _lib.context()
+    ctx.check(ctx.lib.rcg_comm_destroy(ctx.h), "nccl comm destroy")
 
 
 class LoopbackGroup:
