@@ -308,6 +308,9 @@ extern "C" void rcg_ctx_destroy(rcg_ctx* c) {
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.second.exec);
   if (c->dargs) cudaFree(c->dargs);
   if (c->capture_stream) cudaStreamDestroy(c->capture_stream);
+  if (c->halo_stream) cudaStreamDestroy(c->halo_stream);
+  if (c->halo_fork) cudaEventDestroy(c->halo_fork);
+  if (c->halo_join) cudaEventDestroy(c->halo_join);
   if (c->scratch) {
     if (pool_guard()) guard_release(c->scratch);
     else cudaFree(c->scratch);

@@ -212,7 +212,7 @@ __global__ void halo_pack_kernel(int64_t total, const int32_t* __restrict__ idx,
 // (two virtual slabs in one rank, tests/test_gpu_solver.py) - as a send /
 // recv to self, so the whole pack -> ncclSend/ncclRecv -> unpack path and its
 // CUDA-graph capture can be exercised on one GPU.
-static bool halo_active(const Ctx* c, const rcg_halo* H) {
+bool halo_active(const Ctx* c, const rcg_halo* H) {
   if (!H || !c->comm) return false;
   if (c->comm->nranks > 1) return true;
   return comm_force() && !c->comm->loop && c->comm->comm && H->n_ghost > 0;

@@ -16,5 +16,6 @@ int halo_prepare(Ctx* c, const rcg_halo* H);
 int halo_exchange_dev(Ctx* c, const rcg_halo* H, ColSel src, const SolveState* st, ColSel dst);
 // whether solve-loop batches of a sharded solve may be captured in a graph
 bool comm_graphable(const Ctx* c);
+bool halo_active(const Ctx* c, const rcg_halo* H);   // the exchange really moves data (peers, or a forced self exchange)
 void comm_free(Ctx* c);
 }  // namespace rcg

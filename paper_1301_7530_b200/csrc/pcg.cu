@@ -1841,6 +1841,13 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
           ? 8.0 * (double)A->nnz + 4.0 * (double)A->nnz / 9.0 + 4.0 * (double)(n / 3 + 1) + 16.0 * (double)n
           : 12.0 * (double)A->nnz + (A->row_offsets_64 ? 8.0 : 4.0) * (double)(n + 1) + 16.0 * (double)n;
   static const int use_graphs = env_int("RCG_GRAPHS", 1);
+  // sharded: halo exchange beside the local SpMV (needs the DIA + remainder slab format)
+  const bool halo_overlap = H && env_int("RCG_HALO_OVERLAP", 1) && spmv_has_rem(A) && halo_active(c, H);
+  if (halo_overlap && !c->halo_stream) {
+    RCG_CUDA_F(cudaStreamCreateWithFlags(&c->halo_stream, cudaStreamNonBlocking));
+    RCG_CUDA_F(cudaEventCreateWithFlags(&c->halo_fork, cudaEventDisableTiming));
+    RCG_CUDA_F(cudaEventCreateWithFlags(&c->halo_join, cudaEventDisableTiming));
+  }
   const double halo_bytes = H ? 8.0 * ((double)H->send_off[H->nranks] + (double)H->n_ghost) : 0.0;
   bool direct_now = false;   // set by launch_batch: profile the collectives too
   auto allreduce_p = [&](double* buf, size_t count, int64_t jj) -> int {
@@ -1859,15 +1866,33 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     for (int64_t q = 0; q < B; ++q) {
       const int64_t jj = it0 + q;  // the device-side j unless the solve already stopped
       const double nd = (double)n, js = (double)(jj + 1);
-      if (H) {  // ghosts of w_j from the neighbouring slabs (column at device j: graph-capturable)
-        if (direct) prof_begin(c, RCG_K_HALO, halo_bytes, jj);
-        if ((rc2 = halo_exchange_dev(c, H, a.W, st, a.W))) return rc2;
+      if (halo_overlap && !direct) {
+        // the exchange of w_j's ghosts runs on a second stream beside the local
+        // part of the slab SpMV (block-DIA of the local-local block: it reads
+        // only local x) and joins before the ghost-column remainder; inside a
+        // captured batch this is the fork / join of two captured streams
+        RCG_CUDA(c, cudaEventRecord(c->halo_fork, c->stream));
+        RCG_CUDA(c, cudaStreamWaitEvent(c->halo_stream, c->halo_fork, 0));
+        cudaStream_t main_stream = c->stream;
+        c->stream = c->halo_stream;
+        rc2 = halo_exchange_dev(c, H, a.W, st, a.W);
+        c->stream = main_stream;
+        if (rc2) return rc2;
+        RCG_CUDA(c, cudaEventRecord(c->halo_join, c->halo_stream));
+        if ((rc2 = launch_spmv_ind_main(c, A, &dargs->spmv))) return rc2;
+        RCG_CUDA(c, cudaStreamWaitEvent(c->stream, c->halo_join, 0));
+        if ((rc2 = launch_spmv_ind_rem(c, A, &dargs->spmv))) return rc2;
+      } else {
+        if (H) {  // ghosts of w_j from the neighbouring slabs (column at device j: graph-capturable)
+          if (direct) prof_begin(c, RCG_K_HALO, halo_bytes, jj);
+          if ((rc2 = halo_exchange_dev(c, H, a.W, st, a.W))) return rc2;
+          if (direct) prof_end(c);
+        }
+        // algorithmic bytes per launch (each operand touched once)
+        if (direct) prof_begin(c, RCG_K_SPMV, bytes_spmv, jj);
+        if ((rc2 = launch_spmv_ind(c, A, &dargs->spmv))) return rc2;
         if (direct) prof_end(c);
       }
-      // algorithmic bytes per launch (each operand touched once)
-      if (direct) prof_begin(c, RCG_K_SPMV, bytes_spmv, jj);
-      if ((rc2 = launch_spmv_ind(c, A, &dargs->spmv))) return rc2;
-      if (direct) prof_end(c);
       if ((rc2 = allreduce_p(gSum.ptr, 1, jj))) return rc2;
       if (direct) prof_begin(c, RCG_K_UPDATE, 8.0 * nd * (6 + (store ? 1 : 0)), jj);
       RCG_CUDA(c, launch_k(update_kernel, dim3(nbu_l), dim3(kThreads), 0, c->stream, (const IterArgs*)dargs, 0));
@@ -1955,7 +1980,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
       snprintf(key, sizeof(key), "%p|%lld|%d|%d|%d|%d|%zu|%zu|%d|%d|%lld|%d|%d|%p|%lld", (void*)pre, (long long)n,
                spmv_width(A), nbs, nb, nbu, smem_upd, smem_pre, reorth ? 1 : 0, n_c > NC_INLINE ? 1 : 0,
                (long long)B, A->block + 100 * A->bsr_slice + 10000 * (A->dia_count * 4 + A->dia_block),
-               A->row_offsets_64 + 2 * (int)ceil_div(n_c, 8), (const void*)H,
+               A->row_offsets_64 + 2 * (int)ceil_div(n_c, 8) + (halo_overlap ? 1 << 20 : 0), (const void*)H,
                (long long)(H ? reo_cols() : 0));   // sharded: halo plan and allreduce width
       cudaGraphExec_t exec = nullptr;
       auto gi = c->graphs.find(key);

@@ -75,6 +75,8 @@ struct Ctx {
   size_t halo_recv_cap = 0;
   void* dargs = nullptr;                 // device-resident solve arguments (graph replay)
   cudaStream_t capture_stream = nullptr; // private stream for graph capture
+  cudaStream_t halo_stream = nullptr;    // sharded: the halo exchange runs here beside the local SpMV
+  cudaEvent_t halo_fork = nullptr, halo_join = nullptr;
   struct GraphEntry {
     cudaGraphExec_t exec;
     int64_t kernels;   // kernel launches one replay stands for

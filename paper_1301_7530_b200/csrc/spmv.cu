@@ -1324,7 +1324,23 @@ int launch_spmv(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const 
   return RCG_OK;
 }
 
+bool spmv_has_rem(const rcg_csr* A) { return is_dia(A) && has_rem(A); }
+
+// the ghost-column part of a slab SpMV (after launch_spmv_ind_main and the halo exchange)
+int launch_spmv_ind_rem(Ctx* c, const rcg_csr* A, const SpmvArgs* dargs) {
+  if (!spmv_has_rem(A)) return RCG_OK;
+  RCG_CUDA(c, launch_k(rem_kernel_ind, dim3(rem_grid(c, A)), dim3(kThreads), 0, c->stream, dargs));
+  c->launches++;
+  return RCG_OK;
+}
+
 int launch_spmv_ind(Ctx* c, const rcg_csr* A, const SpmvArgs* dargs) {
+  int rc = launch_spmv_ind_main(c, A, dargs);
+  return rc ? rc : launch_spmv_ind_rem(c, A, dargs);
+}
+
+// the part of the solve-loop SpMV that reads only local x (all of it unless the slab has a remainder list)
+int launch_spmv_ind_main(Ctx* c, const rcg_csr* A, const SpmvArgs* dargs) {
   // one solve-loop kernel per stream format, launched with PDL (launch_k)
   void (*k)(const SpmvArgs*) = nullptr;
   int grid = 1;
@@ -1352,10 +1368,6 @@ int launch_spmv_ind(Ctx* c, const rcg_csr* A, const SpmvArgs* dargs) {
   }
   RCG_CUDA(c, launch_k(k, dim3(grid), dim3(kThreads), smem, c->stream, dargs));
   c->launches++;
-  if (is_dia(A) && has_rem(A)) {   // row slab: add the ghost-column entries
-    RCG_CUDA(c, launch_k(rem_kernel_ind, dim3(rem_grid(c, A)), dim3(kThreads), 0, c->stream, dargs));
-    c->launches++;
-  }
   return RCG_OK;
 }
 

@@ -29,6 +29,10 @@ struct SpmvArgs {
   double* rem_part;      // its block partials (after the main kernel's slots)
 };
 int launch_spmv_ind(Ctx* c, const rcg_csr* A, const SpmvArgs* dargs);
+// a slab with a ghost-column remainder: the local part (reads local x only) and the ghost part
+int launch_spmv_ind_main(Ctx* c, const rcg_csr* A, const SpmvArgs* dargs);
+int launch_spmv_ind_rem(Ctx* c, const rcg_csr* A, const SpmvArgs* dargs);
+bool spmv_has_rem(const rcg_csr* A);
 void spmv_args_fill(const rcg_csr* A, SpmvArgs* s);
 // mode 0: y = A x; 1: y = A x + (x,y) -> out[0]; 2: y = b - A x + (y,y),(b,b) -> out[0..1]
 int launch_spmv(Ctx* c, const rcg_csr* A, int mode, ColSel xs, ColSel ys, const double* b,
