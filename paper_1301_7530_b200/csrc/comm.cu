@@ -207,6 +207,27 @@ __global__ void halo_pack_kernel(int64_t total, const int32_t* __restrict__ idx,
     out[k] = s[idx[k]];
 }
 
+// Solve-loop variants: the column selector and the solve state are read from
+// the device-resident argument block, not passed by value, so a captured batch
+// graph stays valid when a later solve of the sequence has other history
+// buffers or another state block (by value they were baked into the graph:
+// the second system of a sharded sequence then read freed memory).
+__global__ void halo_pack_kernel_ind(int64_t total, const int32_t* __restrict__ idx, const ColSel* __restrict__ srcp,
+                                     const SolveState* const* __restrict__ stp, double* __restrict__ out) {
+  const SolveState* st = *stp;
+  const double* s = srcp->at(st->j);   // when the solve already stopped this packs a stale column: harmless
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = s[idx[k]];
+}
+
+__global__ void halo_unpack_kernel_ind(int64_t n_ghost, int64_t n_local, const double* __restrict__ in,
+                                       const ColSel* __restrict__ dstp, const SolveState* const* __restrict__ stp) {
+  const SolveState* st = *stp;
+  double* d = dstp->at(st->j) + n_local;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n_ghost; k += (int64_t)gridDim.x * blockDim.x)
+    d[k] = in[k];
+}
+
 // The exchange runs with peers, or - RCG_COMM_FORCE=1 on a 1-rank NCCL
 // communicator with a plan that lists ghost copies of the rank's own rows
 // (two virtual slabs in one rank, tests/test_gpu_solver.py) - as a send /
@@ -218,7 +239,16 @@ bool halo_active(const Ctx* c, const rcg_halo* H) {
   return comm_force() && !c->comm->loop && c->comm->comm && H->n_ghost > 0;
 }
 
+static int halo_exchange_impl(Ctx* c, const rcg_halo* H, ColSel src, const SolveState* st, const ColSel* src_d,
+                              const SolveState* const* st_d, double* dst_col);
+
 int halo_exchange(Ctx* c, const rcg_halo* H, ColSel src, const SolveState* st, double* dst_col) {
+  return halo_exchange_impl(c, H, src, st, nullptr, nullptr, dst_col);
+}
+
+// src_d / st_d non-null: the solve-loop form (arguments read from device memory)
+static int halo_exchange_impl(Ctx* c, const rcg_halo* H, ColSel src, const SolveState* st, const ColSel* src_d,
+                              const SolveState* const* st_d, double* dst_col) {
   if (!halo_active(c, H)) return RCG_OK;
   if (c->comm->loop) {
     // loopback: the single send buffer may be repacked only after every rank
@@ -231,7 +261,8 @@ int halo_exchange(Ctx* c, const rcg_halo* H, ColSel src, const SolveState* st, d
   if (total > 0) {
     int64_t g = ceil_div(total, kThreads);
     if (g > 4 * c->num_sms) g = 4 * c->num_sms;
-    halo_pack_kernel<<<(unsigned)g, kThreads, 0, c->stream>>>(total, H->send_idx, src, st, H->send_buf);
+    if (src_d) halo_pack_kernel_ind<<<(unsigned)g, kThreads, 0, c->stream>>>(total, H->send_idx, src_d, st_d, H->send_buf);
+    else halo_pack_kernel<<<(unsigned)g, kThreads, 0, c->stream>>>(total, H->send_idx, src, st, H->send_buf);
     RCG_LAUNCH_CHECK(c);
   }
   if (c->comm->loop) return loop_halo(c, H, dst_col);
@@ -251,18 +282,12 @@ int halo_exchange(Ctx* c, const rcg_halo* H, ColSel src, const SolveState* st, d
   return RCG_OK;
 }
 
-__global__ void halo_unpack_kernel(int64_t n_ghost, int64_t n_local, const double* __restrict__ in, ColSel dst,
-                                   const SolveState* st) {
-  long long j = 0;
-  if (st) j = st->j;
-  double* d = dst.at(j) + n_local;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n_ghost; k += (int64_t)gridDim.x * blockDim.x)
-    d[k] = in[k];
-}
-
 int halo_prepare(Ctx* c, const rcg_halo* H) {
   if (!H || H->n_ghost <= 0 || c->halo_recv_cap >= (size_t)H->n_ghost) return RCG_OK;
   RCG_CUDA(c, cudaStreamSynchronize(c->stream));   // the old buffer may still be read
+  // captured batches hold the staging address in their recv / unpack nodes
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.second.exec);
+  c->graphs.clear();
   if (c->halo_recv) cudaFree(c->halo_recv);
   c->halo_recv = nullptr;
   c->halo_recv_cap = 0;
@@ -271,17 +296,18 @@ int halo_prepare(Ctx* c, const rcg_halo* H) {
   return RCG_OK;
 }
 
-int halo_exchange_dev(Ctx* c, const rcg_halo* H, ColSel src, const SolveState* st, ColSel dst) {
+int halo_exchange_dev(Ctx* c, const rcg_halo* H, const ColSel* src_d, const SolveState* const* st_d,
+                      const ColSel* dst_d) {
   if (!halo_active(c, H)) return RCG_OK;
   if (H->n_ghost > (int64_t)c->halo_recv_cap)
     return set_error(c, RCG_ERR_CONTRACT, "halo staging not prepared (halo_prepare before the solve loop)");
   // received ghosts land at halo_recv + recv_off[q] (the exchange's "column"
   // is halo_recv - n_local), then move into the destination column at j
-  int rc = halo_exchange(c, H, src, st, c->halo_recv - H->n_local);
+  int rc = halo_exchange_impl(c, H, ColSel{}, nullptr, src_d, st_d, c->halo_recv - H->n_local);
   if (rc) return rc;
   if (H->n_ghost > 0) {
     const int g = (int)std::min<int64_t>(ceil_div(H->n_ghost, (int64_t)kThreads), 2 * c->num_sms);
-    halo_unpack_kernel<<<g, kThreads, 0, c->stream>>>(H->n_ghost, H->n_local, c->halo_recv, dst, st);
+    halo_unpack_kernel_ind<<<g, kThreads, 0, c->stream>>>(H->n_ghost, H->n_local, c->halo_recv, dst_d, st_d);
     RCG_LAUNCH_CHECK(c);
   }
   return RCG_OK;

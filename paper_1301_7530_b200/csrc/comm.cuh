@@ -13,7 +13,9 @@ int halo_exchange(Ctx* c, const rcg_halo* H, ColSel src, const SolveState* st, d
 // dst.at(j)[n_local + ...] with j read from st on the device
 // allocate the ctx staging buffer for H's ghosts (outside any graph capture)
 int halo_prepare(Ctx* c, const rcg_halo* H);
-int halo_exchange_dev(Ctx* c, const rcg_halo* H, ColSel src, const SolveState* st, ColSel dst);
+// solve-loop exchange: column selectors and the state pointer are read from device memory (graph-replayable)
+int halo_exchange_dev(Ctx* c, const rcg_halo* H, const ColSel* src_d, const SolveState* const* st_d,
+                      const ColSel* dst_d);
 // whether solve-loop batches of a sharded solve may be captured in a graph
 bool comm_graphable(const Ctx* c);
 bool halo_active(const Ctx* c, const rcg_halo* H);   // the exchange really moves data (peers, or a forced self exchange)

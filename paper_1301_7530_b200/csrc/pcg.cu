@@ -1875,7 +1875,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
         RCG_CUDA(c, cudaStreamWaitEvent(c->halo_stream, c->halo_fork, 0));
         cudaStream_t main_stream = c->stream;
         c->stream = c->halo_stream;
-        rc2 = halo_exchange_dev(c, H, a.W, st, a.W);
+        rc2 = halo_exchange_dev(c, H, &dargs->W, &dargs->st, &dargs->W);
         c->stream = main_stream;
         if (rc2) return rc2;
         RCG_CUDA(c, cudaEventRecord(c->halo_join, c->halo_stream));
@@ -1885,7 +1885,7 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
       } else {
         if (H) {  // ghosts of w_j from the neighbouring slabs (column at device j: graph-capturable)
           if (direct) prof_begin(c, RCG_K_HALO, halo_bytes, jj);
-          if ((rc2 = halo_exchange_dev(c, H, a.W, st, a.W))) return rc2;
+          if ((rc2 = halo_exchange_dev(c, H, &dargs->W, &dargs->st, &dargs->W))) return rc2;
           if (direct) prof_end(c);
         }
         // algorithmic bytes per launch (each operand touched once)
@@ -1977,10 +1977,15 @@ static int solve_impl(rcg_ctx* ctx, const rcg_csr* A, const double* inv_diag, co
     } else if (graph_ok) {
       // one graph per (shape, batch size): parameters are all device-resident
       char key[256];
-      snprintf(key, sizeof(key), "%p|%lld|%d|%d|%d|%d|%zu|%zu|%d|%d|%lld|%d|%d|%p|%lld", (void*)pre, (long long)n,
+      // (sharded: the halo plan enters by its device buffers and sizes, which the send / recv / pack nodes
+      //  bake in, not by the host struct's address, which a later plan may reuse)
+      snprintf(key, sizeof(key), "%p|%lld|%d|%d|%d|%d|%zu|%zu|%d|%d|%lld|%d|%d|%p|%p|%p|%lld|%lld|%lld", (void*)pre, (long long)n,
                spmv_width(A), nbs, nb, nbu, smem_upd, smem_pre, reorth ? 1 : 0, n_c > NC_INLINE ? 1 : 0,
                (long long)B, A->block + 100 * A->bsr_slice + 10000 * (A->dia_count * 4 + A->dia_block),
-               A->row_offsets_64 + 2 * (int)ceil_div(n_c, 8) + (halo_overlap ? 1 << 20 : 0), (const void*)H,
+               A->row_offsets_64 + 2 * (int)ceil_div(n_c, 8) + (halo_overlap ? 1 << 20 : 0),
+               (const void*)(H ? H->send_idx : nullptr), (const void*)(H ? H->send_buf : nullptr),
+               (const void*)(H ? gSum.ptr : nullptr),   // the allreduce nodes' buffer (a per-solve pool block)
+               (long long)(H ? H->n_ghost : 0), (long long)(H ? H->send_off[H->nranks] : 0),
                (long long)(H ? reo_cols() : 0));   // sharded: halo plan and allreduce width
       cudaGraphExec_t exec = nullptr;
       auto gi = c->graphs.find(key);
