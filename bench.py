@@ -276,7 +276,15 @@ def device_systems(args, rank=0, world=1, sharded=False):
     nelem, count, kind, _ = shape(args)
     out = []
     for A, b in problems.elasticity_sequence(nelem, count, seed=0, kind=kind, device=True):
-        if sharded:
+        if sharded and world == 1:
+            # --shard-one: two virtual slabs in the one rank (halo exchange with itself, distributed.py)
+            from paper_1301_7530_b200 import distributed as D
+            cut = 3 * ((A.n // 3) // 2)
+            ro_l, lci, va, plan = D.virtual_slab_system(A.row_offsets, A.col_indices, A.values, cut)
+            n_global = A.n
+            A.release_device()
+            A = D.ShardedMatrix(ro_l, lci, va, plan, n_global)
+        elif sharded:
             from paper_1301_7530_b200 import distributed as D
             ro = A.row_offsets
             bounds = D.partition_rows(ro, world, align=3)

@@ -32,7 +32,7 @@ from . import _lib
 from .core import ContractViolation, SparseSpdMatrix
 
 __all__ = ["partition_rows", "HaloPlan", "build_local_system", "local_systems_all", "ShardedMatrix", "init_comm",
-           "destroy_comm",
+           "destroy_comm", "virtual_slab_system",
            "init_loopback", "LoopbackGroup", "nccl_library"]
 
 
@@ -137,6 +137,28 @@ def build_local_system(ro, ci, va, bounds, rank, group=None, gathered=None):
     send_idx = np.concatenate(send_lists).astype(np.int32) if send_off[-1] else np.zeros(0, np.int32)
     plan = HaloPlan(nranks, rank, n_local, len(ghosts), send_idx, send_off, recv_off, ghosts)
     return (ro - ro[0]), lci.astype(np.int32), np.asarray(va, dtype=np.float64), plan
+
+
+def virtual_slab_system(row_offsets, col_indices, values, cut):
+    """One rank's rows cut into two virtual slabs at row ``cut``: couplings
+    between the slabs read ghost copies of the rank's OWN entries (listed
+    after the n local columns), so the rank exchanges a halo with itself.
+    The operator is unchanged.  With ``RCG_COMM_FORCE=1`` on a 1-rank NCCL
+    communicator the exchange is an ncclSend / ncclRecv to self: the whole
+    sharded iteration (pack, NCCL, unpack, slab SpMV, allreduces, graph
+    capture) then runs on one GPU (tests, ``bench.py --shard-one``).
+    Returns (ro, lci, va, plan) like ``build_local_system``."""
+    ro = np.asarray(row_offsets, dtype=np.int64)
+    ci = np.asarray(col_indices, dtype=np.int64)
+    n = len(ro) - 1
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ro))
+    cross = (rows < cut) != (ci < cut)
+    ghosts = np.unique(ci[cross])
+    lci = ci.copy()
+    lci[cross] = n + np.searchsorted(ghosts, ci[cross])
+    off = np.array([0, len(ghosts)], dtype=np.int64)
+    plan = HaloPlan(1, 0, n, len(ghosts), ghosts.astype(np.int32), off, off.copy(), ghosts)
+    return ro - ro[0], lci.astype(np.int32), np.asarray(values, dtype=np.float64), plan
 
 
 class ShardedMatrix(SparseSpdMatrix):
