@@ -124,3 +124,28 @@ def test_slab_local_block_plus_ghost_remainder(kind):
         got = LL @ xe[:nl] + t
         want = y[bounds[r]:bounds[r + 1]]
         np.testing.assert_allclose(got, want, rtol=1e-13, atol=1e-13 * np.abs(want).max())
+
+
+@pytest.mark.parametrize("kind", ["elasticity", "diffusion"])
+def test_virtual_slab_system_is_the_same_operator(kind):
+    """distributed.virtual_slab_system (two virtual slabs in one rank, the
+    one-GPU stand-in for a peer halo): with the ghost region filled from the
+    rank's own entries the extended local system reproduces A x, the plan
+    sends exactly the ghosts it receives, and the local-local block is
+    block-diagonal in the two slabs (so it keeps the symmetric DIA format)."""
+    import scipy.sparse as sp
+    from paper_1301_7530_b200.distributed import virtual_slab_system
+    A, _, align = _problem(kind)
+    n = A.n
+    cut = align * ((n // align) // 2)
+    ro, lci, va, plan = virtual_slab_system(A.row_offsets, A.col_indices, A.values, cut)
+    assert plan.nranks == 1 and plan.n_local == n and plan.n_ghost > 0
+    assert np.array_equal(plan.send_idx, plan.ghost_global) and plan.send_off[-1] == plan.recv_off[-1] == plan.n_ghost
+    S = sp.csr_matrix((va, lci, ro), shape=(n, n + plan.n_ghost))
+    LL = S[:, :n].tocsr()
+    assert abs(LL - LL.T).max() == 0.0
+    assert LL[:cut, cut:].nnz == 0 and LL[cut:, :cut].nnz == 0
+    G = sp.csr_matrix((A.values, A.col_indices, A.row_offsets), shape=(n, n))
+    x = np.random.default_rng(12).standard_normal(n)
+    xe = np.concatenate([x, x[plan.send_idx]])               # the self exchange
+    np.testing.assert_allclose(S @ xe, G @ x, rtol=1e-13, atol=1e-13 * np.abs(G @ x).max())
