@@ -149,18 +149,19 @@ def ghost_remainder_ell(n, row_offsets, col_indices, values):
     slab has no ghost entries.  Host-side (numpy); layout of ``rcg_csr.rem_*``."""
     ro = np.asarray(row_offsets, dtype=np.int64)
     ci = np.asarray(col_indices)
-    ghost = ci >= n
-    if not ghost.any():
+    pos = np.flatnonzero(ci >= n)                 # a few percent of the entries: everything below is on these only
+    if len(pos) == 0:
         return None
-    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ro))[ghost]
+    rows = np.searchsorted(ro, pos, side="right") - 1
     ids, first, counts = np.unique(rows, return_index=True, return_counts=True)
     width, nrow = int(counts.max()), len(ids)
     slot = np.arange(len(rows)) - np.repeat(first, counts)
     srow = np.repeat(np.arange(nrow), counts)
-    eci = np.full((width, nrow), int(ci[ghost][0]), dtype=np.int32)
+    gci = ci[pos]
+    eci = np.full((width, nrow), int(gci[0]), dtype=np.int32)
     eva = np.zeros((width, nrow), dtype=np.float64)
-    eci[slot, srow] = ci[ghost]
-    eva[slot, srow] = np.asarray(values, dtype=np.float64)[ghost]
+    eci[slot, srow] = gci
+    eva[slot, srow] = np.asarray(values)[pos]
     return ids.astype(np.int32), eci, eva
 
 
