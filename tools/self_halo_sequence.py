@@ -1,3 +1,5 @@
+"""A recycling sequence through the sharded path on one GPU (two virtual slabs, NCCL send/recv to self).
+usage: RCG_SHARDED_GRAPHS=0|1 RCG_HALO_OVERLAP=0|1 python tools/self_halo_sequence.py [srks|trks]"""
 import os, sys, socket
 sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1]))
 os.environ["RCG_DIA_SMALL"]="1"; os.environ["RCG_COMM_FORCE"]="1"
@@ -17,7 +19,7 @@ off = np.array([0, len(ghosts)], dtype=np.int64)
 plan = Dm.HaloPlan(1, 0, n, len(ghosts), ghosts.astype(np.int32), off, off.copy(), ghosts)
 Dm.init_comm()
 S = Dm.ShardedMatrix(ro, lci.astype(np.int32), va, plan, n)
-strat = rcg.RecycleStrategy("srks", epsilon=1e-10, nc_limit=61)
+strat = rcg.RecycleStrategy(sys.argv[1] if len(sys.argv) > 1 else "srks", epsilon=1e-10, nc_limit=61)
 rhs = [b, 0.5 * b + 0.1 * np.random.default_rng(6).standard_normal(n), -b]
 cfg2 = rcg.SolveConfig(tol=1e-8, max_iters=3000)
 r1 = rcg.run_sequence([(S, v) for v in rhs], rcg.Preconditioner.jacobi, strat, cfg2)
